@@ -1,0 +1,181 @@
+/*
+ * edgeforge_b200.h -- C ABI of the B200-native Canny path (libedgeforge_b200.so).
+ *
+ * The reference (edgeforge, pure Python) has no FFI or plugin registry; its
+ * seam is the Python call run_pipeline(img, PipelineConfig) and the stage
+ * functions it sequences.  Each entry point below replaces one of those
+ * reference interfaces (cited as file:line under /root/reference/pkg/src/edgeforge)
+ * and is what a ctypes / cffi / cgo binding of that seam binds.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers
+ *    owned by the caller; "h_" pointers are host pointers.
+ *  - Images are dense row-major frames: frame f, row y, column x lives at
+ *    base + (f*height + y)*width + x.  batch >= 1 frames of height x width.
+ *  - weights: HOST pointer to the 2*radius+1 float64 Gaussian weights, exactly
+ *    GaussianKernel.weights (filtering.py:14-29): symmetric, summing to 1.
+ *  - low/high: absolute thresholds on the raw Sobel magnitude (Thresholds,
+ *    hysteresis.py:26-33): 0 <= low <= high.
+ *  - labels: u8 {0 none, 1 weak, 2 strong} (hysteresis.py:19-21);
+ *    final: u8 {0,1}, the traced edge set (EdgeMap.final as bytes).
+ *  - stream: a cudaStream_t passed as void*; all device work is stream-ordered
+ *    and asynchronous unless stated otherwise.
+ *  - Return value: 0 on success; EF_EINVAL (-1) for invalid arguments (the
+ *    reference raises ValueError), EF_ECUDA (-2) for CUDA failures, EF_ENOMEM
+ *    (-3) when the workspace is too small.  ef_last_error() describes the last
+ *    failure on the calling thread.
+ *  - Thread safety: concurrent calls are safe if each thread uses its own
+ *    stream and workspace.
+ */
+#ifndef EDGEFORGE_B200_H
+#define EDGEFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EF_ABI_VERSION 1
+#define EF_OK 0
+#define EF_EINVAL (-1)
+#define EF_ECUDA (-2)
+#define EF_ENOMEM (-3)
+#define EF_MAX_RADIUS 15
+
+/* Library / error plumbing. */
+int ef_abi_version(void);
+const char* ef_last_error(void);
+
+/* Per-call statistics, accumulated on the device into the workspace and read
+ * back (synchronously) by ef_read_stats. */
+typedef struct ef_stats {
+    int64_t fixups;           /* pixels whose fp32 decision was not certified and
+                                 were recomputed in exact float64               */
+    int64_t ambiguous;        /* orientation within 1e-12 of a sector boundary:
+                                 resolved with the reference's atan2 formula    */
+    int64_t border_nodes;     /* tile-border components entering the union-find */
+    int64_t pending_tiles;    /* tiles finalised after the global merge         */
+} ef_stats;
+
+/* Bytes of device workspace needed by ef_canny_u8 / ef_canny_f64 /
+ * ef_trace_edges for `batch` frames of height x width. */
+size_t ef_workspace_bytes(int64_t batch, int32_t height, int32_t width);
+
+/* Zero the statistics block of a workspace (stream-ordered). */
+int ef_reset_stats(void* d_workspace, size_t workspace_bytes, void* stream);
+/* Synchronise `stream` and copy the statistics out. */
+int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream, ef_stats* h_out);
+
+/* Whole Canny path for u8 frames on the device -- replaces run_pipeline
+ * (bench.py:61-126, operator="canny", explicit Thresholds) for inputs whose
+ * pixels are integers in [0,255] (GrayImage holds them as float64, image.py:23-50).
+ *   gaussian_blur (filtering.py:66-91) + sobel (gradient.py:73-90)
+ *   + non_max_suppress (nms.py:36-55) + double_threshold (hysteresis.py:54-60)
+ *   -> d_labels;  trace_edges (hysteresis.py:63-69) -> d_final.
+ * Fused fp32 stencil with a certified error bound; pixels whose decision is
+ * inside the bound are recomputed in exact float64 in the reference's
+ * operation order, so d_labels/d_final are bit-identical to the reference. */
+int ef_canny_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t width,
+                const double* h_weights, int32_t radius, double low, double high,
+                uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Same path for arbitrary finite float64 pixels (GrayImage.pixels) -- exact
+ * float64 stencil in reference order on the GPU (no fp32 fast path). */
+int ef_canny_f64(const double* d_src, int64_t batch, int32_t height, int32_t width,
+                 const double* h_weights, int32_t radius, double low, double high,
+                 uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Stage 1-4 only (labels, no tracing): the fused classify kernel.
+ * Replaces gaussian_blur + sobel + non_max_suppress + double_threshold. */
+int ef_classify_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t width,
+                   const double* h_weights, int32_t radius, double low, double high,
+                   uint8_t* d_labels, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Hysteresis only -- replaces trace_edges (hysteresis.py:63-69): 8-connected
+ * components of labels != 0 that contain a strong pixel. */
+int ef_trace_edges(const uint8_t* d_labels, int64_t batch, int32_t height, int32_t width,
+                   uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Every float64 intermediate of one frame (keep_intermediates=True,
+ * bench.py:124-125): blurred (GrayImage), gx, gy, magnitude, orientation
+ * (int64 degrees, GradientField gradient.py:19-34), thinned (ThinnedField,
+ * nms.py:13-24) and labels.  Input is u8 (d_src8) or float64 (d_src64); the
+ * other pointer must be NULL.  Any output pointer may be NULL. */
+int ef_stages_f64(const uint8_t* d_src8, const double* d_src64, int32_t height, int32_t width,
+                  const double* h_weights, int32_t radius, double low, double high,
+                  double* d_blurred, double* d_gx, double* d_gy, double* d_magnitude,
+                  int64_t* d_orientation, double* d_thinned, uint8_t* d_labels, void* stream);
+
+/* Exact float64 maximum of the thinned field of one frame -- the reduction in
+ * auto_thresholds (bench.py:51-58).  Writes one double to d_max. */
+int ef_thinned_max(const uint8_t* d_src8, const double* d_src64, int32_t height, int32_t width,
+                   const double* h_weights, int32_t radius, double* d_max, void* stream);
+
+/* Stage-level kernels for the reference's stage API on arbitrary arrays. */
+/* non_max_suppress (nms.py:36-55) on a given magnitude/orientation field. */
+int ef_nms_f64(const double* d_magnitude, const int64_t* d_orientation, int32_t height, int32_t width,
+               double* d_thinned, void* stream);
+/* double_threshold (hysteresis.py:54-60) on a given thinned field. */
+int ef_double_threshold_f64(const double* d_thinned, int64_t n, double low, double high, uint8_t* d_labels,
+                            void* stream);
+/* quantize_orientation_array (gradient.py:37-44): int64 degrees. */
+int ef_quantize_f64(const double* d_gx, const double* d_gy, int64_t n, int64_t* d_orientation, void* stream);
+/* laplacian (gradient.py:96-107): 5-point Laplacian, replicate borders. */
+int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double* d_out, void* stream);
+
+/* Host-buffer entry point (the e2e path a drop-in user calls): copies u8 frames
+ * from h_src to the device, runs ef_canny_u8, and copies labels/final back,
+ * overlapping copies and compute across frame chunks on internal streams.
+ * Pinned host buffers give full PCIe bandwidth.  Synchronous on return. */
+int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_t width,
+                     const double* h_weights, int32_t radius, double low, double high,
+                     uint8_t* h_labels, uint8_t* h_final, int32_t device);
+
+/* ---- Row-band partition of one huge frame (multi-GPU, trace_edges_parallel
+ * hysteresis.py:90-131 generalised across devices). -----------------------
+ *
+ * A band owns rows [row0, row0+rows) of a frame of full_height rows.  d_src
+ * holds rows [row0-halo_top, row0+rows+halo_bot) where
+ * halo_top = min(row0, radius+2) and halo_bot = min(full_height-row0-rows, radius+2):
+ * neighbours' rows arrive by P2P/NCCL, the frame edge is clamped. */
+int ef_band_halo_rows(int32_t radius);
+
+/* Labels of the band plus the band-local hysteresis (tiles, union-find),
+ * leaving components that touch the band's top/bottom edge undecided. */
+int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t full_height,
+                     int32_t width, const double* h_weights, int32_t radius, double low,
+                     double high, uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* Band-local hysteresis only, for labels already computed (the per-band
+ * labelling of trace_edges_parallel, hysteresis.py:97-101). */
+int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* Export the band's two edge rows: for each column of the top and bottom row,
+ * the band-local component id (int64, -1 for background) and whether that
+ * component is already known to hold a strong pixel (u8).  Arrays have
+ * 2*width entries: [0,width) top row, [width,2*width) bottom row. */
+int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows, int32_t width,
+                  int64_t* d_ids, uint8_t* d_strong, void* stream);
+
+/* Host-side cross-band merge (the union-find of hysteresis.py:112-130): given
+ * every band's edge rows in band order (nbands blocks of 2*width entries, ids
+ * already made globally unique), decide which ids end up connected to a strong
+ * pixel.  Writes h_strong_out (same layout as the inputs). */
+int ef_band_merge(int32_t nbands, int32_t width, const int64_t* h_ids, const uint8_t* h_strong,
+                  uint8_t* h_strong_out);
+
+/* Apply the merged decision for this band's edge rows and finalise d_final. */
+int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width,
+                     const uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
+                     size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDGEFORGE_B200_H */

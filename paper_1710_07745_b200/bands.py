@@ -1,0 +1,226 @@
+"""Row-band partition of one frame: within a GPU (trace_edges_parallel) and
+across GPUs (config 4: one 16384^2 image over 2/4/8 B200s).
+
+The reference's template is trace_edges_parallel (hysteresis.py:90-131):
+label each band independently, renumber into one id space, union the
+components that touch across each band seam (shifts -1/0/+1), then keep
+components that reach a strong pixel.  Here:
+
+  band compute   ef_band_canny_u8 (classify + band-local tile union-find) or
+                 ef_band_trace (labels given); components touching the band's
+                 top/bottom row stay undecided.
+  edge export    ef_band_edges: per column of the top and bottom row, the
+                 band-local component root and whether it already holds a
+                 strong pixel.  ids are made global as (band << 40) | root.
+  seam merge     ef_band_merge (host C union-find over at most 2*W*nbands
+                 entries -- tiny next to the image), identical on every rank.
+  finalize       ef_band_finalize: mark merged-strong roots, re-finalise the
+                 tiles that had undecided components.
+
+Multi-GPU (one process per GPU, torch.distributed):
+  halo exchange  each rank owns rows [row0, row0+rows) in HBM and needs
+                 radius+2 rows from each neighbour: batch_isend_irecv over NCCL
+                 (NVLink P2P); frame edges are clamped instead.
+  edge exchange  all_gather of the 2*W edge ids/flags (NCCL).
+The compute steps go through a backend object so that the orchestration runs
+under gloo on CPU in the tests with an oracle-backed backend.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+ID_SHIFT = 40
+
+
+def band_plan(height: int, nbands: int) -> list[tuple[int, int]]:
+    """Near-equal contiguous bands (engine.plan_bands with granularity 1)."""
+    size = -(-height // nbands)
+    return [(s, min(s + size, height)) for s in range(0, height, size)]
+
+
+def halo_rows(radius: int) -> int:
+    return radius + 2  # blur radius + Sobel 1 + NMS 1 (ef_band_halo_rows)
+
+
+def globalize_ids(ids: np.ndarray, band: int) -> np.ndarray:
+    out = ids.astype(np.int64, copy=True)
+    m = out >= 0
+    out[m] = (np.int64(band) << ID_SHIFT) | out[m]
+    return out
+
+
+def merge_edges(ids_all: np.ndarray, strong_all: np.ndarray, width: int) -> np.ndarray:
+    """Host union-find over every band's edge rows (ef_band_merge).
+    ids_all/strong_all: (nbands, 2*width) int64/uint8, ids already global."""
+    nb = ids_all.shape[0]
+    ids = np.ascontiguousarray(ids_all, dtype=np.int64)
+    strong = np.ascontiguousarray(strong_all, dtype=np.uint8)
+    out = np.empty_like(strong)
+    _lib.check(_lib.load().ef_band_merge(nb, width, ids.ctypes.data, strong.ctypes.data, out.ctypes.data),
+               "ef_band_merge")
+    return out
+
+
+class CudaBandBackend:
+    """Band compute on the local CUDA device through the C ABI."""
+
+    def __init__(self, rows: int, width: int):
+        from . import canny
+
+        self.torch = canny.require_cuda()
+        self.canny = canny
+        self.rows, self.width = rows, width
+        self.ws = canny.new_workspace(1, rows, width)
+        self.labels = None
+        self.final = None
+
+    def _stream(self):
+        return int(self.torch.cuda.current_stream().cuda_stream)
+
+    def classify_trace(self, buf, row0: int, full_height: int, weights, low: float, high: float):
+        """buf: u8 CUDA tensor holding rows [row0-ht, row0+rows+hb) of the frame."""
+        t = self.torch
+        self.labels = t.empty((self.rows, self.width), dtype=t.uint8, device=buf.device)
+        self.final = t.empty_like(self.labels)
+        _, wp, r = self.canny.host_weights(weights)
+        rc = _lib.load().ef_band_canny_u8(buf.data_ptr(), row0, self.rows, full_height, self.width, wp, r,
+                                          float(low), float(high), self.labels.data_ptr(), self.final.data_ptr(),
+                                          self.ws.data_ptr(), self.ws.numel(), self._stream())
+        _lib.check(rc, "ef_band_canny_u8")
+
+    def trace(self, labels):
+        t = self.torch
+        self.labels = labels
+        self.final = t.empty_like(labels)
+        rc = _lib.load().ef_band_trace(labels.data_ptr(), self.rows, self.width, self.final.data_ptr(),
+                                       self.ws.data_ptr(), self.ws.numel(), self._stream())
+        _lib.check(rc, "ef_band_trace")
+
+    def edges(self):
+        t = self.torch
+        ids = t.empty(2 * self.width, dtype=t.int64, device=self.labels.device)
+        strong = t.empty(2 * self.width, dtype=t.uint8, device=self.labels.device)
+        rc = _lib.load().ef_band_edges(self.ws.data_ptr(), self.ws.numel(), self.rows, self.width,
+                                       ids.data_ptr(), strong.data_ptr(), self._stream())
+        _lib.check(rc, "ef_band_edges")
+        return ids, strong
+
+    def finalize(self, strong_edges):
+        rc = _lib.load().ef_band_finalize(strong_edges.data_ptr(), self.rows, self.width, self.labels.data_ptr(),
+                                          self.final.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                          self._stream())
+        _lib.check(rc, "ef_band_finalize")
+        return self.final
+
+
+def trace_bands_local(labels, plan: list[tuple[int, int]]):
+    """trace_edges_parallel on one GPU: band-local tracing + host seam merge."""
+    from . import canny
+
+    torch = canny.require_cuda()
+    h, w = labels.shape
+    final = torch.empty_like(labels)
+    backends, ids_all, strong_all = [], [], []
+    for k, (s, e) in enumerate(plan):
+        be = CudaBandBackend(e - s, w)
+        be.trace(labels[s:e])
+        ids, strong = be.edges()
+        backends.append(be)
+        ids_all.append(globalize_ids(ids.cpu().numpy(), k))
+        strong_all.append(strong.cpu().numpy())
+    merged = merge_edges(np.stack(ids_all), np.stack(strong_all), w)
+    for k, ((s, e), be) in enumerate(zip(plan, backends)):
+        fin = be.finalize(torch.from_numpy(merged[k]).to(labels.device))
+        final[s:e].copy_(fin)
+    return final
+
+
+def canny_bands_local(frame_u8, nbands: int, weights, low: float, high: float):
+    """Whole-frame Canny through the band path on one GPU (each band reads its
+    halo from the resident frame) -- the single-device emulation of the
+    multi-GPU partition, used to test the band kernels against ef_canny_u8."""
+    from . import canny
+
+    torch = canny.require_cuda()
+    h, w = frame_u8.shape
+    r = (len(weights) - 1) // 2
+    halo = halo_rows(r)
+    labels = torch.empty_like(frame_u8)
+    final = torch.empty_like(frame_u8)
+    plan = band_plan(h, nbands)
+    backends, ids_all, strong_all = [], [], []
+    for k, (s, e) in enumerate(plan):
+        lo, hi = max(0, s - halo), min(h, e + halo)
+        be = CudaBandBackend(e - s, w)
+        be.classify_trace(frame_u8[lo:hi].contiguous(), s, h, weights, low, high)
+        ids, strong = be.edges()
+        backends.append(be)
+        ids_all.append(globalize_ids(ids.cpu().numpy(), k))
+        strong_all.append(strong.cpu().numpy())
+    merged = merge_edges(np.stack(ids_all), np.stack(strong_all), w)
+    for k, ((s, e), be) in enumerate(zip(plan, backends)):
+        final[s:e].copy_(be.finalize(torch.from_numpy(merged[k]).to(frame_u8.device)))
+        labels[s:e].copy_(be.labels)
+    return labels, final
+
+
+def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: float, high: float,
+                           backend=None, group=None):
+    """One rank's share of a row-band-partitioned frame.
+
+    band_u8: this rank's rows [row0, row0+rows) as a (rows, W) u8 tensor on the
+    rank's device (CUDA under NCCL, CPU under gloo with a test backend).
+    Returns (labels, final) for those rows, equal to the rows of the
+    whole-frame result."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rows, w = band_u8.shape
+    r = (len(weights) - 1) // 2
+    halo = halo_rows(r)
+    # neighbour row counts are needed to know how many halo rows they can give
+    counts = [torch.zeros(2, dtype=torch.int64, device=band_u8.device) for _ in range(world)]
+    dist.all_gather(counts, torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), group=group)
+    meta = [(int(c[0]), int(c[1])) for c in counts]
+    ht = min(halo, row0)
+    hb = min(halo, full_height - row0 - rows)
+    buf = torch.empty((ht + rows + hb, w), dtype=torch.uint8, device=band_u8.device)
+    buf[ht:ht + rows].copy_(band_u8)
+    # halo exchange (a halo may span several thin neighbour bands)
+    ops = []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        p0, pr = meta[peer]
+        # rows of mine that the peer needs: its halo window intersected with my rows
+        need0, need1 = max(0, p0 - halo), min(full_height, p0 + pr + halo)
+        s0, s1 = max(need0, row0), min(need1, row0 + rows)
+        if s0 < s1 and not (p0 <= s0 and s1 <= p0 + pr):
+            ops.append(dist.P2POp(dist.isend, band_u8[s0 - row0:s1 - row0].contiguous(), peer, group))
+        # rows of the peer that I need
+        g0, g1 = max(p0, row0 - ht), min(p0 + pr, row0 + rows + hb)
+        if g0 < g1 and not (row0 <= g0 and g1 <= row0 + rows):
+            dst = buf[g0 - (row0 - ht):g1 - (row0 - ht)]
+            ops.append(dist.P2POp(dist.irecv, dst, peer, group))
+    recvd = []
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    del recvd
+    be = backend if backend is not None else CudaBandBackend(rows, w)
+    be.classify_trace(buf, row0, full_height, weights, low, high)
+    ids, strong = be.edges()
+    gids = torch.from_numpy(globalize_ids(ids.cpu().numpy(), rank)).to(band_u8.device)
+    ids_l = [torch.empty_like(gids) for _ in range(world)]
+    st_l = [torch.empty_like(strong) for _ in range(world)]
+    dist.all_gather(ids_l, gids, group=group)
+    dist.all_gather(st_l, strong, group=group)
+    ids_all = np.stack([t.cpu().numpy() for t in ids_l])
+    st_all = np.stack([t.cpu().numpy() for t in st_l])
+    merged = merge_edges(ids_all, st_all, w)
+    fin = be.finalize(torch.from_numpy(merged[rank]).to(band_u8.device))
+    return be.labels, fin

@@ -1,0 +1,581 @@
+// ef_abi.cu -- the extern "C" surface of libedgeforge_b200.so (include/edgeforge_b200.h).
+//
+// Host responsibilities: argument validation with the reference's error
+// semantics (ValueError -> EF_EINVAL), the certified fp32 error bounds for the
+// fast path, workspace layout, kernel sequencing, the host-buffer pipeline and
+// the cross-band union-find.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "ef_common.cuh"
+#include "ef_internal.h"
+
+using namespace ef;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return EF_ECUDA;
+}
+
+#define EF_CHECK(call, what)                          \
+    do {                                              \
+        cudaError_t _e = (call);                      \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+int sm_count_current() {
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n;
+    return n;
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct WsLayout {
+    size_t hdr, fix, perim, gpar, gstrong, pending, total;
+    unsigned long long fix_cap;
+    HystLayout hl;
+};
+
+WsLayout ws_layout(int64_t batch, int H, int W) {
+    WsLayout L;
+    L.hl = hyst_layout(batch, H, W);
+    unsigned long long npx = (unsigned long long)batch * H * W;
+    L.fix_cap = std::max<unsigned long long>(1ull << 16, npx / 64);
+    size_t off = 0;
+    L.hdr = off;
+    off = align_up(off + sizeof(WsHeader));
+    L.fix = off;
+    off = align_up(off + L.fix_cap * sizeof(unsigned long long));
+    L.perim = off;
+    off = align_up(off + (size_t)L.hl.slots * sizeof(int));
+    L.gpar = off;
+    off = align_up(off + (size_t)L.hl.slots * sizeof(int));
+    L.gstrong = off;
+    off = align_up(off + (size_t)L.hl.slots);
+    L.pending = off;
+    off = align_up(off + (size_t)L.hl.tiles);
+    L.total = off;
+    return L;
+}
+
+struct Ws {
+    WsHeader* hdr;
+    unsigned long long* fix;
+    HystBufs hb;
+};
+
+Ws ws_bind(void* base, const WsLayout& L) {
+    char* p = static_cast<char*>(base);
+    Ws w;
+    w.hdr = reinterpret_cast<WsHeader*>(p + L.hdr);
+    w.fix = reinterpret_cast<unsigned long long*>(p + L.fix);
+    w.hb.perim = reinterpret_cast<int*>(p + L.perim);
+    w.hb.gpar = reinterpret_cast<int*>(p + L.gpar);
+    w.hb.gstrong = reinterpret_cast<uint8_t*>(p + L.gstrong);
+    w.hb.pending = reinterpret_cast<uint8_t*>(p + L.pending);
+    return w;
+}
+
+__global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap) {
+    hdr->fix_count = 0;
+    hdr->fix_cap = cap;
+    hdr->overflow = 0;
+}
+
+__global__ void ws_reset_stats_kernel(WsHeader* hdr) {
+    hdr->stats.fixups = 0;
+    hdr->stats.ambiguous = 0;
+    hdr->stats.border_nodes = 0;
+    hdr->stats.pending_tiles = 0;
+}
+
+int check_dims(int64_t batch, int32_t H, int32_t W) {
+    if (batch < 1 || H < 1 || W < 1)
+        return fail(EF_EINVAL, "image dimensions must be >= 1, got batch=" + std::to_string(batch) + " " +
+                                   std::to_string(W) + "x" + std::to_string(H));
+    if ((unsigned long long)batch * H * W > (1ull << 40)) return fail(EF_EINVAL, "image too large");
+    if ((long long)((W + 63) / 64) * ((H + 63) / 64) * batch * 256 >= (1ll << 31))
+        return fail(EF_EINVAL, "too many tiles for 32-bit node ids; split the batch");
+    return EF_OK;
+}
+
+// GaussianKernel validation (filtering.py:20-29) plus the threshold validation
+// (hysteresis.py:31-33).
+int check_params(const double* w, int32_t r, double low, double high) {
+    if (!w) return fail(EF_EINVAL, "weights pointer is NULL");
+    if (r < 0 || r > EF_MAX_RADIUS)
+        return fail(EF_EINVAL, "radius must be in [0, " + std::to_string(EF_MAX_RADIUS) + "], got " +
+                                   std::to_string(r));
+    double sum = 0.0;
+    for (int i = 0; i <= 2 * r; ++i) {
+        if (!std::isfinite(w[i])) return fail(EF_EINVAL, "kernel weights must be finite");
+        if (w[i] != w[2 * r - i]) return fail(EF_EINVAL, "kernel weights must be symmetric");
+        sum += w[i];
+    }
+    if (std::fabs(sum - 1.0) > 1e-9) return fail(EF_EINVAL, "kernel weights must sum to 1");
+    if (!(0.0 <= low && low <= high))
+        return fail(EF_EINVAL, "need 0 <= low <= high, got low=" + std::to_string(low) +
+                                   ", high=" + std::to_string(high));
+    return EF_OK;
+}
+
+ExactParams make_exact(const double* w, int r, double low, double high) {
+    ExactParams P;
+    std::memset(&P, 0, sizeof P);
+    for (int i = 0; i <= 2 * r; ++i) P.w[i] = w[i];
+    P.r = r;
+    P.low = low;
+    P.high = high;
+    return P;
+}
+
+// Certified bounds of the fp32 fast path.  u8
+// inputs: |b| <= 255, |gx|,|gy| <= 1020, magnitude <= 1442.5.
+FastParams make_fast(const double* w, int r, double low, double high) {
+    FastParams P;
+    std::memset(&P, 0, sizeof P);
+    P.r = r;
+    for (int k = 0; k <= r; ++k) P.wf[k] = (float)w[r + k];
+    const double u = std::ldexp(1.0, -24), u64 = std::ldexp(1.0, -53);
+    const double eh = (r + 2) * u * 255.0;                                  // horizontal pass
+    const double eb = eh + (r + 3) * u * 255.0 + (4 * r + 6) * u64 * 255.0;  // vertical pass (+f64 side)
+    const double eg = 8.0 * eb + 4080.0 * u + 12.0 * u64 * 1020.0 + 1e-9;   // Sobel
+    const double rel = std::ldexp(1.0, -20) + 3.0 * u;                      // m^2 rounding + sqrt.approx
+    const double S = 2.0;                                                   // safety factor
+    auto Em = [&](double M) { return std::sqrt(2.0) * eg + rel * M + 1e-9; };
+    auto band = [&](double T, float& lo, float& hi) {
+        if (!(T > 0.0)) {  // every magnitude is >= 0 >= T
+            lo = hi = -1.0f;
+            return;
+        }
+        double e = S * Em(T + 1.0);
+        lo = std::nextafter((float)(T - e), -INFINITY);
+        hi = std::nextafter((float)(T + e), INFINITY);
+    };
+    band(low, P.lo_lo, P.lo_hi);
+    band(high, P.hi_lo, P.hi_hi);
+    P.e_nms = (float)(S * 2.0 * Em(1443.0 * 1.01));
+    P.e_sec = (float)(S * ((1.0 + 0.41421356237309503) * eg + 3000.0 * u));
+    P.cls0 = high <= 0.0 ? 2 : (low <= 0.0 ? 1 : 0);
+    return P;
+}
+
+FrameGeom frame_geom(int H, int W) { return FrameGeom{H, W, 0, H, 0, H}; }
+
+bool has_negative(const double* w, int r) {
+    for (int i = 0; i <= 2 * r; ++i)
+        if (w[i] < 0.0) return true;
+    return false;
+}
+
+int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const double* w, int r,
+                    double low, double high, uint8_t* labels, const Ws& ws, const WsLayout& L,
+                    cudaStream_t st) {
+    int sms = sm_count_current();
+    if (has_negative(w, r)) {
+        // the certified bounds assume a convex (non-negative) kernel; a signed
+        // kernel takes the exact float64 kernel instead
+        if (g.g0 != 0 || g.full_H != g.H || g.rows != g.H) return fail(EF_EINVAL, "signed kernel on a band");
+        ExactParams XP = make_exact(w, r, low, high);
+        EF_CHECK(launch_exact<uint8_t>(src, batch, g.H, g.W, XP, labels, nullptr, nullptr, nullptr, nullptr,
+                                       nullptr, nullptr, nullptr, ws.hdr, st),
+                 "exact kernel");
+        return EF_OK;
+    }
+    ws_begin_kernel<<<1, 1, 0, st>>>(ws.hdr, L.fix_cap);
+    EF_CHECK(cudaGetLastError(), "ws_begin");
+    FastParams FP = make_fast(w, r, low, high);
+    EF_CHECK(launch_k1(src, batch, g, FP, labels, ws.fix, ws.hdr, st), "classify kernel");
+    ExactParams XP = make_exact(w, r, low, high);
+    EF_CHECK(launch_fix(src, batch, g, XP, labels, ws.fix, ws.hdr, sms, st), "fix-up kernel");
+    return EF_OK;
+}
+
+int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws,
+              cudaStream_t st, bool finalize) {
+    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, sm_count_current(), st),
+             "hysteresis");
+    if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, st), "hysteresis finalize");
+    return EF_OK;
+}
+
+int check_ws(void* ws, size_t bytes, const WsLayout& L) {
+    if (!ws) return fail(EF_EINVAL, "workspace pointer is NULL");
+    if (bytes < L.total)
+        return fail(EF_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes, got " +
+                                   std::to_string(bytes));
+    return EF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ef_abi_version(void) { return EF_ABI_VERSION; }
+
+const char* ef_last_error(void) { return g_err.c_str(); }
+
+size_t ef_workspace_bytes(int64_t batch, int32_t height, int32_t width) {
+    if (batch < 1 || height < 1 || width < 1) return 0;
+    return ws_layout(batch, height, width).total;
+}
+
+int ef_reset_stats(void* d_workspace, size_t workspace_bytes, void* stream) {
+    if (!d_workspace || workspace_bytes < sizeof(WsHeader)) return fail(EF_EINVAL, "bad workspace");
+    ws_reset_stats_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<WsHeader*>(d_workspace));
+    EF_CHECK(cudaGetLastError(), "reset stats");
+    return EF_OK;
+}
+
+int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream, ef_stats* h_out) {
+    if (!d_workspace || workspace_bytes < sizeof(WsHeader) || !h_out) return fail(EF_EINVAL, "bad arguments");
+    EF_CHECK(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+    EF_CHECK(cudaMemcpy(h_out, d_workspace, sizeof(ef_stats), cudaMemcpyDeviceToHost), "stats copy");
+    return EF_OK;
+}
+
+int ef_classify_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t width,
+                   const double* h_weights, int32_t radius, double low, double high, uint8_t* d_labels,
+                   void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (!d_src || !d_labels) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(batch, height, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    return run_classify_u8(d_src, batch, frame_geom(height, width), h_weights, radius, low, high, d_labels, ws,
+                           L, (cudaStream_t)stream);
+}
+
+int ef_canny_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
+                int32_t radius, double low, double high, uint8_t* d_labels, uint8_t* d_final,
+                void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (!d_src || !d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(batch, height, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = run_classify_u8(d_src, batch, frame_geom(height, width), h_weights, radius, low, high, d_labels,
+                              ws, L, st)))
+        return rc;
+    return run_trace(d_labels, batch, height, width, d_final, ws, st, true);
+}
+
+int ef_canny_f64(const double* d_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
+                 int32_t radius, double low, double high, uint8_t* d_labels, uint8_t* d_final,
+                 void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (!d_src || !d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(batch, height, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    cudaStream_t st = (cudaStream_t)stream;
+    ExactParams XP = make_exact(h_weights, radius, low, high);
+    EF_CHECK(launch_exact<double>(d_src, batch, height, width, XP, d_labels, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr, nullptr, ws.hdr, st),
+             "exact kernel");
+    return run_trace(d_labels, batch, height, width, d_final, ws, st, true);
+}
+
+int ef_trace_edges(const uint8_t* d_labels, int64_t batch, int32_t height, int32_t width, uint8_t* d_final,
+                   void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(batch, height, width))) return rc;
+    if (!d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(batch, height, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    return run_trace(d_labels, batch, height, width, d_final, ws, (cudaStream_t)stream, true);
+}
+
+int ef_stages_f64(const uint8_t* d_src8, const double* d_src64, int32_t height, int32_t width,
+                  const double* h_weights, int32_t radius, double low, double high, double* d_blurred,
+                  double* d_gx, double* d_gy, double* d_magnitude, int64_t* d_orientation, double* d_thinned,
+                  uint8_t* d_labels, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if ((d_src8 == nullptr) == (d_src64 == nullptr)) return fail(EF_EINVAL, "exactly one source pointer");
+    ExactParams XP = make_exact(h_weights, radius, low, high);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (d_src8)
+        EF_CHECK(launch_exact<uint8_t>(d_src8, 1, height, width, XP, d_labels, d_blurred, d_gx, d_gy, d_magnitude,
+                                       d_orientation, d_thinned, nullptr, nullptr, st),
+                 "exact kernel");
+    else
+        EF_CHECK(launch_exact<double>(d_src64, 1, height, width, XP, d_labels, d_blurred, d_gx, d_gy, d_magnitude,
+                                      d_orientation, d_thinned, nullptr, nullptr, st),
+                 "exact kernel");
+    return EF_OK;
+}
+
+int ef_thinned_max(const uint8_t* d_src8, const double* d_src64, int32_t height, int32_t width,
+                   const double* h_weights, int32_t radius, double* d_max, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, height, width)) || (rc = check_params(h_weights, radius, 0.0, 0.0))) return rc;
+    if ((d_src8 == nullptr) == (d_src64 == nullptr) || !d_max) return fail(EF_EINVAL, "bad buffers");
+    ExactParams XP = make_exact(h_weights, radius, 0.0, 0.0);
+    cudaStream_t st = (cudaStream_t)stream;
+    EF_CHECK(cudaMemsetAsync(d_max, 0, sizeof(double), st), "memset");
+    auto* bits = reinterpret_cast<unsigned long long*>(d_max);
+    if (d_src8)
+        EF_CHECK(launch_exact<uint8_t>(d_src8, 1, height, width, XP, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                       nullptr, nullptr, bits, nullptr, st),
+                 "exact kernel");
+    else
+        EF_CHECK(launch_exact<double>(d_src64, 1, height, width, XP, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                      nullptr, nullptr, bits, nullptr, st),
+                 "exact kernel");
+    return EF_OK;
+}
+
+int ef_nms_f64(const double* d_magnitude, const int64_t* d_orientation, int32_t height, int32_t width,
+               double* d_thinned, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, height, width))) return rc;
+    if (!d_magnitude || !d_orientation || !d_thinned) return fail(EF_EINVAL, "NULL buffer");
+    EF_CHECK(launch_nms(d_magnitude, d_orientation, height, width, d_thinned, nullptr, (cudaStream_t)stream),
+             "nms kernel");
+    return EF_OK;
+}
+
+int ef_double_threshold_f64(const double* d_thinned, int64_t n, double low, double high, uint8_t* d_labels,
+                            void* stream) {
+    if (n < 0 || (n && (!d_thinned || !d_labels))) return fail(EF_EINVAL, "bad buffers");
+    if (!(0.0 <= low && low <= high)) return fail(EF_EINVAL, "need 0 <= low <= high");
+    if (n) EF_CHECK(launch_threshold(d_thinned, n, low, high, d_labels, (cudaStream_t)stream), "threshold kernel");
+    return EF_OK;
+}
+
+int ef_quantize_f64(const double* d_gx, const double* d_gy, int64_t n, int64_t* d_orientation, void* stream) {
+    if (n < 0 || (n && (!d_gx || !d_gy || !d_orientation))) return fail(EF_EINVAL, "bad buffers");
+    if (n) EF_CHECK(launch_quantize(d_gx, d_gy, n, d_orientation, (cudaStream_t)stream), "quantize kernel");
+    return EF_OK;
+}
+
+int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double* d_out, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, height, width))) return rc;
+    if (!d_src || !d_out) return fail(EF_EINVAL, "NULL buffer");
+    EF_CHECK(launch_laplacian(d_src, height, width, d_out, (cudaStream_t)stream), "laplacian kernel");
+    return EF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline: chunks of frames round-robin over two streams so the
+// H2D copy of chunk i+1, the kernels of chunk i and the D2H of chunk i-1
+// overlap (separate copy engines).
+// ---------------------------------------------------------------------------
+namespace {
+struct HostCtx {
+    std::mutex mu;
+    int dev = -1;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    uint8_t* buf[2] = {nullptr, nullptr};  // src | labels | final per stream
+    void* ws[2] = {nullptr, nullptr};
+    size_t buf_px = 0, ws_bytes = 0;
+};
+
+HostCtx& host_ctx(int dev) {
+    static std::mutex mu;
+    static std::unordered_map<int, HostCtx*> ctxs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& p = ctxs[dev];
+    if (!p) p = new HostCtx();
+    return *p;
+}
+}  // namespace
+
+int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
+                     int32_t radius, double low, double high, uint8_t* h_labels, uint8_t* h_final,
+                     int32_t device) {
+    int rc;
+    if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (!h_src || !h_labels || !h_final) return fail(EF_EINVAL, "NULL buffer");
+    EF_CHECK(cudaSetDevice(device), "cudaSetDevice");
+    HostCtx& C = host_ctx(device);
+    std::lock_guard<std::mutex> lk(C.mu);
+    const size_t fpx = (size_t)height * width;
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)((8u << 20) / fpx)));
+    if (batch >= 2 && chunk >= batch) chunk = (batch + 1) / 2;
+    const size_t need_px = (size_t)chunk * fpx;
+    const size_t need_ws = ef_workspace_bytes(chunk, height, width);
+    if (C.dev != device) {
+        C.dev = device;
+        for (int i = 0; i < 2; ++i) EF_CHECK(cudaStreamCreateWithFlags(&C.st[i], cudaStreamNonBlocking), "stream");
+    }
+    if (C.buf_px < need_px || C.ws_bytes < need_ws) {
+        for (int i = 0; i < 2; ++i) {
+            if (C.buf[i]) cudaFree(C.buf[i]);
+            if (C.ws[i]) cudaFree(C.ws[i]);
+            C.buf[i] = nullptr;
+            C.ws[i] = nullptr;
+        }
+        for (int i = 0; i < 2; ++i) {
+            EF_CHECK(cudaMalloc(&C.buf[i], 3 * need_px), "cudaMalloc");
+            EF_CHECK(cudaMalloc(&C.ws[i], need_ws), "cudaMalloc");
+        }
+        C.buf_px = need_px;
+        C.ws_bytes = need_ws;
+    }
+    int k = 0;
+    for (int64_t f0 = 0; f0 < batch; f0 += chunk, k ^= 1) {
+        int64_t n = std::min<int64_t>(chunk, batch - f0);
+        size_t bytes = (size_t)n * fpx;
+        cudaStream_t st = C.st[k];
+        uint8_t* d_src = C.buf[k];
+        uint8_t* d_lab = d_src + C.buf_px;
+        uint8_t* d_fin = d_lab + C.buf_px;
+        EF_CHECK(cudaMemcpyAsync(d_src, h_src + f0 * fpx, bytes, cudaMemcpyHostToDevice, st), "H2D");
+        if ((rc = ef_canny_u8(d_src, n, height, width, h_weights, radius, low, high, d_lab, d_fin, C.ws[k],
+                              C.ws_bytes, st)))
+            return rc;
+        EF_CHECK(cudaMemcpyAsync(h_labels + f0 * fpx, d_lab, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        EF_CHECK(cudaMemcpyAsync(h_final + f0 * fpx, d_fin, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    EF_CHECK(cudaStreamSynchronize(C.st[0]), "sync");
+    EF_CHECK(cudaStreamSynchronize(C.st[1]), "sync");
+    return EF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row bands (multi-GPU partition of one frame).
+// ---------------------------------------------------------------------------
+int ef_band_halo_rows(int32_t radius) { return radius + 2; }
+
+int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t full_height, int32_t width,
+                     const double* h_weights, int32_t radius, double low, double high, uint8_t* d_labels,
+                     uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, rows, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (row0 < 0 || row0 + rows > full_height) return fail(EF_EINVAL, "band outside the frame");
+    if (!d_src || !d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(1, rows, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    const int halo = radius + 2;
+    const int ht = std::min(row0, halo), hb = std::min(full_height - row0 - rows, halo);
+    FrameGeom g{ht + rows + hb, width, row0 - ht, full_height, row0, rows};
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = run_classify_u8(d_src, 1, g, h_weights, radius, low, high, d_labels, ws, L, st))) return rc;
+    return run_trace(d_labels, 1, rows, width, d_final, ws, st, false);
+}
+
+int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,
+                  size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, rows, width))) return rc;
+    if (!d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    WsLayout L = ws_layout(1, rows, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    return run_trace(d_labels, 1, rows, width, d_final, ws, (cudaStream_t)stream, false);
+}
+
+int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows, int32_t width, int64_t* d_ids,
+                  uint8_t* d_strong, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, rows, width))) return rc;
+    WsLayout L = ws_layout(1, rows, width);
+    if ((rc = check_ws(const_cast<void*>(d_workspace), workspace_bytes, L))) return rc;
+    if (!d_ids || !d_strong) return fail(EF_EINVAL, "NULL buffer");
+    Ws ws = ws_bind(const_cast<void*>(d_workspace), L);
+    EF_CHECK(launch_band_edges(rows, width, ws.hb, d_ids, d_strong, (cudaStream_t)stream), "band edges");
+    return EF_OK;
+}
+
+int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width, const uint8_t* d_labels,
+                     uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, rows, width))) return rc;
+    WsLayout L = ws_layout(1, rows, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    if (!d_strong_edges || !d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    Ws ws = ws_bind(d_workspace, L);
+    cudaStream_t st = (cudaStream_t)stream;
+    EF_CHECK(launch_band_apply(rows, width, ws.hb, d_strong_edges, st), "band apply");
+    EF_CHECK(launch_hyst_final(d_labels, 1, rows, width, d_final, ws.hb, st), "hysteresis finalize");
+    return EF_OK;
+}
+
+// Serial union-find over the band-edge components, the analogue of
+// hysteresis.py:112-130 (pairs at shifts -1/0/+1 across each band seam).
+int ef_band_merge(int32_t nbands, int32_t width, const int64_t* h_ids, const uint8_t* h_strong,
+                  uint8_t* h_strong_out) {
+    if (nbands < 1 || width < 1 || !h_ids || !h_strong || !h_strong_out) return fail(EF_EINVAL, "bad arguments");
+    const size_t n = (size_t)nbands * 2 * width;
+    std::unordered_map<int64_t, int> index;
+    index.reserve(n);
+    std::vector<int> parent;
+    std::vector<uint8_t> strong;
+    std::vector<int> slot(n, -1);
+    for (size_t i = 0; i < n; ++i) {
+        if (h_ids[i] < 0) continue;
+        auto it = index.find(h_ids[i]);
+        int id;
+        if (it == index.end()) {
+            id = (int)parent.size();
+            index.emplace(h_ids[i], id);
+            parent.push_back(id);
+            strong.push_back(0);
+        } else {
+            id = it->second;
+        }
+        slot[i] = id;
+        if (h_strong[i]) strong[id] = 1;
+    }
+    auto find = [&](int a) {
+        while (parent[a] != a) {
+            parent[a] = parent[parent[a]];
+            a = parent[a];
+        }
+        return a;
+    };
+    for (int b = 0; b + 1 < nbands; ++b) {
+        const int* top = &slot[(size_t)b * 2 * width + width];   // bottom row of band b
+        const int* bot = &slot[(size_t)(b + 1) * 2 * width];     // top row of band b+1
+        for (int x = 0; x < width; ++x) {
+            if (top[x] < 0) continue;
+            for (int s = -1; s <= 1; ++s) {
+                int x2 = x + s;
+                if (x2 < 0 || x2 >= width || bot[x2] < 0) continue;
+                int ra = find(top[x]), rb = find(bot[x2]);
+                if (ra != rb) {
+                    parent[rb] = ra;
+                    strong[ra] = strong[ra] | strong[rb];
+                }
+            }
+        }
+    }
+    for (size_t i = 0; i < n; ++i) h_strong_out[i] = slot[i] < 0 ? 0 : strong[find(slot[i])];
+    return EF_OK;
+}
+
+}  // extern "C"

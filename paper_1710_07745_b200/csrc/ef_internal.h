@@ -1,0 +1,67 @@
+// ef_internal.h -- launcher declarations shared by the .cu files.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ef {
+
+struct ExactParams;
+struct FastParams;
+struct WsHeader;
+
+// geometry of one frame or one row band of a frame (see ef_band_* in the ABI)
+struct FrameGeom {
+    int H;       // rows held in the source buffer
+    int W;       // columns
+    int g0;      // global row of source row 0
+    int full_H;  // rows of the whole frame (clamping is against [0, full_H))
+    int out0;    // first global row to classify
+    int rows;    // rows to classify; output row (Y - out0)
+};
+
+struct HystLayout {
+    int tiles_x, tiles_y;
+    int64_t tiles, slots;
+};
+
+struct HystBufs {
+    int* perim;
+    int* gpar;
+    uint8_t* gstrong;
+    uint8_t* pending;
+};
+
+size_t ex_smem_bytes(int r);
+size_t k1_smem_bytes(int r);
+
+template <typename In>
+cudaError_t launch_exact(const In* src, int64_t batch, int H, int W, const ExactParams& P,
+                         uint8_t* labels, double* blurred, double* gx, double* gy, double* mag,
+                         int64_t* ori, double* thin, unsigned long long* max_bits, WsHeader* hdr,
+                         cudaStream_t st);
+
+cudaError_t launch_k1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
+                      uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
+
+cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
+                       uint8_t* labels, const unsigned long long* list, WsHeader* hdr, int sm_count,
+                       cudaStream_t st);
+
+HystLayout hyst_layout(int64_t batch, int H, int W);
+cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
+                              const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st);
+cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
+                              const HystBufs& b, cudaStream_t st);
+cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
+                              cudaStream_t st);
+cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,
+                              cudaStream_t st);
+
+cudaError_t launch_nms(const double* mag, const int64_t* ori, int H, int W, double* thin, int* bad, cudaStream_t st);
+cudaError_t launch_threshold(const double* thin, long long n, double low, double high, uint8_t* labels,
+                             cudaStream_t st);
+cudaError_t launch_quantize(const double* gx, const double* gy, long long n, int64_t* ori, cudaStream_t st);
+cudaError_t launch_laplacian(const double* src, int H, int W, double* out, cudaStream_t st);
+
+}  // namespace ef

@@ -1,0 +1,161 @@
+"""run_pipeline -- the drop-in for the reference's Canny entry point
+(bench.py:20-140): same PipelineConfig / PipelineResult surface, computed by
+the sm_100a kernels of libedgeforge_b200.so.
+
+Paths:
+  * integer pixels in [0, 255] (every config and PGM input): the fused fp32
+    classify kernel with certified decisions + exact float64 fix-ups +
+    tile union-find hysteresis (ef_canny_u8_host: H2D, kernels, D2H);
+  * any other finite float64 pixels: the exact float64 stencil kernel in the
+    reference's operation order + the same hysteresis (ef_canny_f64).
+Both give labels/final bit-identical to the reference.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import StageTiming, WorkerConfig
+from .filtering import GaussianKernel, build_gaussian_kernel
+from .gradient import GradientField
+from .hysteresis import EdgeMap, Thresholds, trace_edges_parallel
+from .image import GrayImage
+from .nms import ThinnedField
+
+AUTO_HIGH_RATIO = 0.2  # high = ratio * max thinned magnitude (bench.py:20)
+AUTO_LOW_RATIO = 0.4  # low = ratio * high (bench.py:21)
+WORKER_HARD_CAP = 64
+
+
+@dataclass
+class PipelineConfig:
+    sigma: float = 1.4
+    thresholds: Thresholds | None = None  # None = auto ratios from the thinned field
+    workers: WorkerConfig = field(default_factory=WorkerConfig)
+    hysteresis_mode: str = "serial"  # serial | parallel
+    operator: str = "canny"  # canny | laplacian
+    radius: int | None = None  # Gaussian radius; None = ceil(3*sigma) as the reference
+
+    def __post_init__(self):
+        if self.hysteresis_mode not in ("serial", "parallel"):
+            raise ValueError(f"unknown hysteresis mode {self.hysteresis_mode!r}")
+        if self.operator not in ("canny", "laplacian"):
+            raise ValueError(f"unknown operator {self.operator!r}")
+        if self.radius is not None and self.radius < 0:
+            raise ValueError(f"radius must be >= 0, got {self.radius}")
+
+    def kernel(self) -> GaussianKernel:
+        return build_gaussian_kernel(self.sigma, self.radius)
+
+
+@dataclass
+class PipelineResult:
+    edges: EdgeMap | None = None
+    response: GrayImage | None = None  # laplacian operator output
+    blurred: GrayImage | None = None
+    grad: GradientField | None = None
+    thinned: ThinnedField | None = None
+    thresholds: Thresholds | None = None
+
+
+def auto_thresholds(thin: ThinnedField) -> Thresholds:
+    """bench.py:51-58: high = 0.2 * max thinned magnitude, low = 0.4 * high."""
+    return _auto_from_peak(float(thin.magnitude.max()))
+
+
+def _auto_from_peak(peak: float) -> Thresholds:
+    if peak == 0.0:
+        return Thresholds(low=1.0, high=1.0)
+    high = AUTO_HIGH_RATIO * peak
+    return Thresholds(low=AUTO_LOW_RATIO * high, high=high)
+
+
+def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming] | None = None,
+                 band_times: dict[str, list[list[int]]] | None = None,
+                 keep_intermediates: bool = False) -> PipelineResult:
+    """blur -> sobel -> nms -> threshold -> trace (or blur -> laplacian), on the GPU.
+
+    Output is bit-identical to the reference for the same inputs and config.
+    ``timings`` receives one StageTiming per device phase ("canny" for the
+    fused path, "laplacian"); ``band_times`` is accepted for signature
+    compatibility (there are no CPU bands)."""
+    from . import canny
+
+    torch = canny.require_cuda()
+    clock = time.perf_counter_ns
+    kernel = cfg.kernel()
+    w = kernel.weights
+    result = PipelineResult()
+    px = img.pixels
+    u8 = img.as_u8()
+
+    def record(stage: str, t0: int):
+        if timings is not None:
+            timings.append(StageTiming(stage_name=stage, workers=cfg.workers.workers,
+                                       wall_ns=clock() - t0, rows_processed=img.height))
+
+    if cfg.operator == "laplacian":
+        t0 = clock()
+        src = torch.from_numpy(np.ascontiguousarray(px)).cuda()
+        blurred = canny.blur_f64(src, w)
+        result.response = GrayImage.from_array(canny.laplacian_f64(blurred).cpu().numpy())
+        record("laplacian", t0)
+        if keep_intermediates:
+            result.blurred = GrayImage.from_array(blurred.cpu().numpy())
+        return result
+
+    t0 = clock()
+    dev_src = None
+    thresholds = cfg.thresholds
+    if thresholds is None or keep_intermediates:
+        dev_src = torch.from_numpy(u8 if u8 is not None else np.ascontiguousarray(px)).cuda()
+    if thresholds is None:
+        thresholds = _auto_from_peak(canny.thinned_max(dev_src, w))
+    if u8 is not None and cfg.hysteresis_mode == "serial":
+        labels, final = canny.canny_u8_host(u8, w, thresholds.low, thresholds.high)
+    else:
+        if dev_src is None:
+            dev_src = torch.from_numpy(u8 if u8 is not None else np.ascontiguousarray(px)).cuda()
+        if u8 is not None:
+            lab_d = canny.classify_u8(dev_src, w, thresholds.low, thresholds.high)[0]
+        else:
+            lab_d = canny.canny_f64(dev_src, w, thresholds.low, thresholds.high)[0][0]
+        if cfg.hysteresis_mode == "parallel":
+            from . import bands
+            from .engine import plan_bands
+
+            fin_d = bands.trace_bands_local(lab_d, plan_bands(img.height, cfg.workers))
+        else:
+            fin_d = canny.trace_edges_u8(lab_d)[0]
+        labels, final = lab_d.cpu().numpy(), fin_d.cpu().numpy()
+    record("canny", t0)
+    edges = EdgeMap(width=img.width, height=img.height, labels=np.ascontiguousarray(labels),
+                    final=np.ascontiguousarray(final).view(np.bool_))
+    result.edges = edges
+    result.thresholds = thresholds
+    if keep_intermediates:
+        st = canny.stages_f64(dev_src, w, thresholds.low, thresholds.high)
+        h = {k: v.cpu().numpy() for k, v in st.items()}
+        result.blurred = GrayImage.from_array(h["blurred"])
+        result.grad = GradientField(width=img.width, height=img.height, gx=h["gx"], gy=h["gy"],
+                                    magnitude=h["magnitude"], orientation=h["orientation"])
+        result.thinned = ThinnedField(width=img.width, height=img.height, magnitude=h["thinned"])
+    return result
+
+
+def edges_to_image(edges: EdgeMap) -> GrayImage:
+    """Binary edge map as a 0/255 image (bench.py:129-133)."""
+    if edges.final is None:
+        raise ValueError("edge map has not been traced")
+    return GrayImage.from_array(np.where(edges.final, 255.0, 0.0))
+
+
+def rescale_for_view(arr: np.ndarray) -> GrayImage:
+    """Linear rescale of |values| to [0, 255] (bench.py:136-140)."""
+    mag = np.abs(np.asarray(arr, dtype=np.float64))
+    peak = mag.max()
+    return GrayImage.from_array(mag * (255.0 / peak) if peak > 0 else mag)

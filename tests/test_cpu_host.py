@@ -1,0 +1,160 @@
+"""CPU-side tests: the C-ABI library loads and exports what include/*.h
+declares, host-side logic (band plan, seam union-find, validation, PGM), and
+that the product refuses to run without a CUDA device (no CPU fallback)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1710_07745_b200 as ef
+from paper_1710_07745_b200 import _lib, bands
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _declared_symbols():
+    names = set()
+    inc = os.path.join(ROOT, "include")
+    for f in os.listdir(inc):
+        if f.endswith(".h"):
+            text = open(os.path.join(inc, f)).read()
+            names |= set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(ef_\w+)\(", text, re.M))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.exported_symbols())
+    assert lib.ef_abi_version() == 1
+
+
+def test_workspace_sizes_are_positive_and_monotone():
+    lib = _lib.load()
+    a = lib.ef_workspace_bytes(1, 1080, 1920)
+    b = lib.ef_workspace_bytes(64, 1080, 1920)
+    assert 0 < a < b
+    assert lib.ef_workspace_bytes(0, 10, 10) == 0
+    assert lib.ef_band_halo_rows(2) == 4 and lib.ef_band_halo_rows(5) == 7
+
+
+def _py_merge(ids_all, strong_all, width):
+    parent = {}
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    strong = {}
+    for ids, st in zip(ids_all, strong_all):
+        for i, s in zip(ids, st):
+            if i >= 0:
+                parent.setdefault(i, i)
+                strong[i] = strong.get(i, 0) | int(s)
+    for k in range(len(ids_all) - 1):
+        top, bot = ids_all[k][width:], ids_all[k + 1][:width]
+        for x in range(width):
+            for s in (-1, 0, 1):
+                if 0 <= x + s < width and top[x] >= 0 and bot[x + s] >= 0:
+                    a, b = find(top[x]), find(bot[x + s])
+                    if a != b:
+                        parent[b] = a
+    root_strong = {}
+    for i in parent:
+        root_strong[find(i)] = root_strong.get(find(i), 0) | strong[i]
+    return np.array([[root_strong[find(i)] if i >= 0 else 0 for i in ids] for ids in ids_all], np.uint8)
+
+
+def test_band_merge_host_matches_python_union_find():
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        nb, w = int(rng.integers(1, 6)), int(rng.integers(1, 40))
+        ids_all = []
+        for k in range(nb):
+            local = rng.integers(-1, 6, size=2 * w)
+            ids_all.append(bands.globalize_ids(local, k))
+        ids_all = np.stack(ids_all)
+        strong = (rng.random(ids_all.shape) < 0.15).astype(np.uint8)
+        strong[ids_all < 0] = 0
+        # a component's strong flag is per id: make it consistent
+        for k in range(nb):
+            for i in np.unique(ids_all[k]):
+                if i >= 0:
+                    strong[k][ids_all[k] == i] = strong[k][ids_all[k] == i].max()
+        got = bands.merge_edges(ids_all, strong, w)
+        assert np.array_equal(got, _py_merge(ids_all, strong, w)), trial
+
+
+def test_band_plan_and_ids():
+    assert bands.band_plan(10, 3) == [(0, 4), (4, 8), (8, 10)]
+    assert bands.band_plan(16384, 8)[-1] == (14336, 16384)
+    g = bands.globalize_ids(np.array([-1, 0, 5]), 3)
+    assert g[0] == -1 and g[1] == 3 << 40 and g[2] == (3 << 40) | 5
+    assert ef.plan_bands(10, ef.WorkerConfig(workers=4, band_granularity=1)) == [(0, 3), (3, 6), (6, 9), (9, 10)]
+
+
+def test_reference_api_validation():
+    with pytest.raises(ValueError):
+        ef.Thresholds(low=5.0, high=2.0)
+    with pytest.raises(ValueError):
+        ef.Thresholds(low=-1.0, high=2.0)
+    with pytest.raises(ValueError):
+        ef.PipelineConfig(hysteresis_mode="bogus")
+    with pytest.raises(ValueError):
+        ef.PipelineConfig(operator="sobel")
+    with pytest.raises(ValueError):
+        ef.build_gaussian_kernel(0.0)
+    with pytest.raises(ValueError):
+        ef.GaussianKernel(sigma=1.0, radius=1, weights=np.array([0.2, 0.5, 0.3]))
+    k = ef.build_gaussian_kernel(1.4)
+    assert k.radius == 5 and len(k.weights) == 11  # ceil(3 * 1.4) = 5, filtering.py:36
+    assert ef.build_gaussian_kernel(1.4, radius=2).weights.shape == (5,)
+    assert ef.PipelineConfig().kernel().radius == 5
+    with pytest.raises(ValueError):
+        ef.GrayImage.from_array(np.array([[np.nan]]))
+    with pytest.raises(ValueError):
+        ef.EdgeMap(width=2, height=2, labels=np.zeros((3, 3), np.uint8))
+
+
+def test_grayimage_u8_detection():
+    assert ef.GrayImage.from_array(np.array([[0.0, 255.0]])).as_u8() is not None
+    assert ef.GrayImage.from_array(np.array([[0.5, 1.0]])).as_u8() is None
+    assert ef.GrayImage.from_array(np.array([[256.0]])).as_u8() is None
+    assert ef.GrayImage.from_array(np.array([[-1.0]])).as_u8() is None
+
+
+def test_pgm_roundtrip_and_errors():
+    rng = np.random.default_rng(1)
+    arr = rng.integers(0, 256, (7, 9)).astype(np.float64)
+    img = ef.GrayImage.from_array(arr)
+    back = ef.load_pgm(ef.save_pgm(img))
+    assert np.array_equal(back.pixels, arr)
+    assert np.array_equal(ef.load_pgm(b"P2\n2 1\n255\n3 4\n").pixels, [[3.0, 4.0]])
+    with pytest.raises(ef.PgmFormatError):
+        ef.load_pgm(b"P6\n1 1\n255\n\x00")
+    with pytest.raises(ef.PgmFormatError):
+        ef.load_pgm(b"P5\n4 4\n255\n\x00\x00")
+
+
+def test_edges_to_image_and_auto_thresholds():
+    em = ef.EdgeMap(width=2, height=1, labels=np.array([[2, 0]], np.uint8), final=np.array([[True, False]]))
+    assert ef.edges_to_image(em).pixels.tolist() == [[255.0, 0.0]]
+    t = ef.auto_thresholds(ef.ThinnedField(width=3, height=1, magnitude=np.array([[0.0, 10.0, 5.0]])))
+    assert (t.low, t.high) == (0.4 * (0.2 * 10.0), 0.2 * 10.0)
+    assert ef.auto_thresholds(ef.ThinnedField(width=1, height=1, magnitude=np.zeros((1, 1)))).high == 1.0
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    img = ef.GrayImage.from_array(np.zeros((4, 4)))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        ef.run_pipeline(img, ef.PipelineConfig(thresholds=ef.Thresholds(1.0, 2.0)))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        ef.trace_edges(ef.EdgeMap(width=1, height=1, labels=np.zeros((1, 1), np.uint8)))

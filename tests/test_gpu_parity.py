@@ -1,0 +1,257 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+and the reference-generated golden fixtures.  Bar: bit-exact labels and final
+edge sets (integer work); float64 intermediates bit-exact as well.
+"""
+
+import numpy as np
+import pytest
+
+from golden_data import load, unpack
+from oracle import oracle as O
+from paper_1710_07745_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def canny():
+    from paper_1710_07745_b200 import canny as c
+
+    c.require_cuda()
+    return c
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------- golden ----
+@pytest.mark.parametrize("cfg", range(5))
+@pytest.mark.parametrize("r", [2, 5])
+def test_configs_match_reference_golden(canny, cfg, r):
+    g = load("configs.npz")
+    frames = synth.make_config(cfg, reduced=True)
+    assert synth.sha256_u8(frames) == str(g[f"c{cfg}/sha256"])
+    low, high = synth.CONFIG_THRESHOLDS[cfg]
+    w = g[f"c{cfg}/r{r}/weights"]
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high)
+    assert np.array_equal(_np(lab), g[f"c{cfg}/r{r}/labels"])
+    assert np.array_equal(_np(fin).astype(bool), unpack(g[f"c{cfg}/r{r}/final"], frames.shape))
+
+
+def test_stages_match_reference_golden(canny):
+    g = load("stages.npz")
+    for name in [str(n) for n in g["names"]]:
+        arr = g[f"{name}/input"]
+        low, high = g[f"{name}/thresholds"]
+        st = canny.stages_f64(_dev(arr), g[f"{name}/weights"], low, high)
+        for key in ("blurred", "gx", "gy", "magnitude", "orientation", "thinned", "labels"):
+            assert np.array_equal(_np(st[key]), g[f"{name}/{key}"]), (name, key)
+        if np.array_equal(arr, np.floor(arr)) and arr.min() >= 0 and arr.max() <= 255:
+            lab, fin = canny.canny_u8(_dev(arr.astype(np.uint8)), g[f"{name}/weights"], low, high)
+            assert np.array_equal(_np(lab)[0], g[f"{name}/labels"]), name
+            assert np.array_equal(_np(fin)[0].astype(bool), g[f"{name}/final"]), name
+        lab, fin = canny.canny_f64(_dev(arr), g[f"{name}/weights"], low, high)
+        assert np.array_equal(_np(lab)[0], g[f"{name}/labels"]), name
+        assert np.array_equal(_np(fin)[0].astype(bool), g[f"{name}/final"]), name
+
+
+def test_dropin_run_pipeline_matches_reference_golden():
+    import paper_1710_07745_b200 as ef
+
+    g = load("pipeline.npz")
+    for name in [str(n) for n in g["names"]]:
+        arr = g[f"{name}/input"]
+        img = ef.GrayImage.from_array(arr)
+        for tag, thr in (("t2050", ef.Thresholds(20.0, 50.0)), ("auto", None), ("t00", ef.Thresholds(0.0, 0.0)),
+                         ("t0_30", ef.Thresholds(0.0, 30.0)), ("tbig", ef.Thresholds(1e9, 1e9))):
+            res = ef.run_pipeline(img, ef.PipelineConfig(sigma=1.4, thresholds=thr))
+            assert np.array_equal(res.edges.labels, g[f"{name}/{tag}/labels"]), (name, tag)
+            assert np.array_equal(res.edges.final, unpack(g[f"{name}/{tag}/final"], arr.shape)), (name, tag)
+            assert (res.thresholds.low, res.thresholds.high) == tuple(g[f"{name}/{tag}/thresholds"]), (name, tag)
+        res = ef.run_pipeline(img, ef.PipelineConfig(thresholds=ef.Thresholds(20.0, 50.0), hysteresis_mode="parallel",
+                                                     workers=ef.WorkerConfig(workers=3, band_granularity=2)))
+        assert np.array_equal(res.edges.final, unpack(g[f"{name}/t2050/final"], arr.shape)), name
+
+
+# ------------------------------------------------------- random vs oracle ----
+def _random_image(rng, h, w, kind):
+    if kind == "noise":
+        return rng.integers(0, 256, (h, w)).astype(np.uint8)
+    if kind == "blocks":
+        blk = rng.integers(0, 2, (h // 8 + 1, w // 8 + 1)) * 255
+        return np.kron(blk, np.ones((8, 8)))[:h, :w].astype(np.uint8)
+    y, x = np.mgrid[0:h, 0:w]
+    return ((x * 7 + y * 3) % 256).astype(np.uint8)
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 3, 5, 8, 15])
+def test_fast_path_random_vs_oracle(canny, r):
+    rng = np.random.default_rng(100 + r)
+    sigma = max(0.3, r / 3.0)
+    w = O.gaussian_weights(sigma, radius=r)
+    shapes = [(1, 1), (1, 37), (29, 1), (2, 3), (31, 65), (64, 64), (97, 130), (200, 333)]
+    for (h, wd) in shapes:
+        for kind in ("noise", "blocks", "ramp"):
+            img = _random_image(rng, h, wd, kind)
+            low = float(rng.choice([0.0, 5.0, 20.0, 100.0]))
+            high = low + float(rng.choice([0.0, 10.0, 40.0, 300.0]))
+            lab, fin = canny.canny_u8(_dev(img), w, low, high)
+            el, ef_ = O.canny(img, w, low, high)
+            assert np.array_equal(_np(lab)[0], el), (r, h, wd, kind, low, high)
+            assert np.array_equal(_np(fin)[0].astype(bool), ef_), (r, h, wd, kind, low, high)
+
+
+def test_float_path_random_vs_oracle(canny):
+    rng = np.random.default_rng(5)
+    for (h, wd) in [(1, 1), (7, 5), (33, 47), (128, 96)]:
+        img = rng.random((h, wd)) * 300.0 - 20.0
+        w = O.gaussian_weights(1.4)
+        lab, fin = canny.canny_f64(_dev(img), w, 10.0, 40.0)
+        el, ef_ = O.canny(img, w, 10.0, 40.0)
+        assert np.array_equal(_np(lab)[0], el)
+        assert np.array_equal(_np(fin)[0].astype(bool), ef_)
+
+
+def test_batch_of_frames_vs_oracle(canny):
+    frames = synth.config1(3, 135, 241)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    el, ef_ = O.canny(frames, w, 20.0, 50.0, threads=8)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+    for i in range(3):  # batch invariance
+        l1, f1 = canny.canny_u8(_dev(frames[i]), w, 20.0, 50.0)
+        assert np.array_equal(_np(l1)[0], _np(lab)[i])
+        assert np.array_equal(_np(f1)[0], _np(fin)[i])
+
+
+# ----------------------------------------------------------- hysteresis -----
+def _snake(h, w):
+    lab = np.zeros((h, w), np.uint8)
+    for y in range(0, h, 2):
+        lab[y, :] = 1
+        if y + 1 < h:
+            lab[y + 1, (w - 1) if (y // 2) % 2 == 0 else 0] = 1
+    lab[h - 1 - ((h - 1) % 2), 0] = 2
+    return lab
+
+
+def _spiral_labels(n):
+    lab = np.zeros((n, n), np.uint8)
+    y, x, dy, dx = 0, 0, 0, 1
+    seen = np.zeros((n, n), bool)
+    for _ in range(n * n):
+        lab[y, x] = 1
+        seen[y, x] = True
+        ny, nx = y + 2 * dy, x + 2 * dx
+        if not (0 <= ny < n and 0 <= nx < n) or seen[ny, nx]:
+            dy, dx = dx, -dy
+            ny, nx = y + 2 * dy, x + 2 * dx
+            if not (0 <= ny < n and 0 <= nx < n) or seen[ny, nx]:
+                break
+        lab[y + dy, x + dx] = 1
+        seen[y + dy, x + dx] = True
+        y, x = ny, nx
+    lab[y, x] = 2
+    return lab
+
+
+def test_hysteresis_vs_oracle(canny):
+    rng = np.random.default_rng(3)
+    cases = [_snake(300, 257), _spiral_labels(333), _snake(64, 64), _snake(65, 129)]
+    for p in ([0.55, 0.35, 0.10], [0.3, 0.65, 0.05], [0.9, 0.09, 0.01]):
+        for (h, w) in [(1, 1), (1, 200), (200, 1), (63, 65), (128, 128), (517, 389)]:
+            cases.append(rng.choice([0, 1, 2], size=(h, w), p=p).astype(np.uint8))
+    for lab in cases:
+        fin = canny.trace_edges_u8(_dev(lab))
+        assert np.array_equal(_np(fin)[0].astype(bool), O.trace(lab)), lab.shape
+    # the snake and the spiral are single components reaching every tile
+    assert _np(canny.trace_edges_u8(_dev(_spiral_labels(333))))[0].sum() == (_spiral_labels(333) != 0).sum()
+
+
+def test_band_paths_match_whole_frame(canny):
+    from paper_1710_07745_b200 import bands
+
+    frame = synth.config4(1024, tile=256)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frame), w, 20.0, 50.0)
+    for nb in (2, 3, 8):
+        bl, bf = bands.canny_bands_local(_dev(frame), nb, w, 20.0, 50.0)
+        assert np.array_equal(_np(bl), _np(lab)[0]), nb
+        assert np.array_equal(_np(bf), _np(fin)[0]), nb
+    snake = _snake(300, 257)
+    ref = O.trace(snake)
+    for plan in ([(0, 100), (100, 300)], [(0, 7), (7, 8), (8, 150), (150, 300)]):
+        got = bands.trace_bands_local(_dev(snake), plan)
+        assert np.array_equal(_np(got).astype(bool), ref), plan
+
+
+def test_host_buffer_entry_matches_device(canny):
+    frames = synth.config3(3, 256)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    hl, hf = canny.canny_u8_host(frames, w, 20.0, 50.0)
+    assert np.array_equal(hl, _np(lab)) and np.array_equal(hf, _np(fin))
+
+
+def test_invalid_arguments_raise_valueerror(canny):
+    w = O.gaussian_weights(1.4)
+    img = _dev(np.zeros((8, 8), np.uint8))
+    with pytest.raises(ValueError):
+        canny.canny_u8(img, w, 50.0, 20.0)
+    with pytest.raises(ValueError):
+        canny.canny_u8(img, np.array([0.2, 0.5, 0.3]), 1.0, 2.0)
+    with pytest.raises(ValueError):
+        canny.canny_u8(img, np.ones(33) / 33, 1.0, 2.0)
+
+
+# --------------------------------------------------- full-size configs ------
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_full_size_configs_vs_oracle(canny, cfg):
+    frames = synth.make_config(cfg)
+    low, high = synth.CONFIG_THRESHOLDS[cfg]
+    w = O.gaussian_weights(1.4, radius=2)
+    ws = canny.new_workspace(*frames.shape)
+    canny.reset_stats(ws)
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high, ws=ws)
+    stats = canny.read_stats(ws)
+    el, ef_ = O.canny(frames, w, low, high, threads=0)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+    print(f"config {cfg}: {frames.size} px, stats {stats}")
+
+
+def test_full_size_config4_band_invariance(canny):
+    from paper_1710_07745_b200 import bands
+
+    frame = synth.config4()
+    w = O.gaussian_weights(1.4, radius=2)
+    d = _dev(frame)
+    lab, fin = canny.canny_u8(d, w, 20.0, 50.0)
+    el, ef_ = O.canny(frame, w, 20.0, 50.0, threads=0)
+    assert np.array_equal(_np(lab)[0], el)
+    assert np.array_equal(_np(fin)[0].astype(bool), ef_)
+    bl, bf = bands.canny_bands_local(d, 8, w, 20.0, 50.0)
+    assert torch.equal(bl, lab[0]) and torch.equal(bf, fin[0])
+
+
+def test_full_size_config3_subset_and_properties(canny):
+    frames = synth.config3(48)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    el, ef_ = O.canny(frames, w, 20.0, 50.0, threads=0)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+    # properties: strong pixels are final, final pixels are labelled, and a
+    # stricter high threshold never adds edges
+    L, F = _np(lab), _np(fin).astype(bool)
+    assert F[L == 2].all() and not F[L == 0].any()
+    _, fin2 = canny.canny_u8(_dev(frames), w, 20.0, 80.0)
+    assert not (_np(fin2).astype(bool) & ~F).any()
