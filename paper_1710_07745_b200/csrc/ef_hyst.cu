@@ -134,8 +134,9 @@ __device__ void tile_ccl(const uint8_t* __restrict__ labels, int H, int W, const
     const uint8_t* frame = labels + (size_t)g.f * H * W;
     const int Y = g.y0 + row;
     uint8_t v[16];
-    if (row < g.vh && seg + 16 <= g.vw && ((((size_t)Y * W + g.x0 + seg) & 15) == 0)) {
-        uint4 q = *reinterpret_cast<const uint4*>(frame + (size_t)Y * W + g.x0 + seg);
+    const uint8_t* src = frame + (size_t)Y * W + g.x0 + seg;
+    if (row < g.vh && seg + 16 <= g.vw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        uint4 q = *reinterpret_cast<const uint4*>(src);
         const uint8_t* qb = reinterpret_cast<const uint8_t*>(&q);
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = qb[k];
@@ -178,17 +179,23 @@ __device__ void tile_ccl(const uint8_t* __restrict__ labels, int H, int W, const
         }
     }
     __syncthreads();
-    // flatten, strong flags, perimeter minima
-#pragma unroll 1
+    // roots, strong flags, perimeter minima.  Roots go to registers first:
+    // concurrent path-halving writes could otherwise overwrite a stored root
+    // with a non-root ancestor; the forest is only rewritten after a barrier.
+    int roots[16];
+#pragma unroll
     for (int k = 0; k < 16; ++k) {
         int x = seg + k, i = row * HT + x;
+        roots[k] = v[k] ? sfind(s.par, i) : -1;
         if (!v[k]) continue;
-        int root = sfind(s.par, i);
-        s.par[i] = root;
-        if (v[k] == kStrong) s.sflag[root] = 1;
+        if (v[k] == kStrong) s.sflag[roots[k]] = 1;
         int p = perim_slot(row, x, g.vh, g.vw);
-        if (p != NO_POS) atomicMin(&s.minpos[root], p);
+        if (p != NO_POS) atomicMin(&s.minpos[roots[k]], p);
     }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (v[k]) s.par[row * HT + seg + k] = roots[k];
     __syncthreads();
 }
 
@@ -206,7 +213,7 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
     uint8_t* frame = final_out + (size_t)g.f * H * W;
     bool pend = false;
     if (row < g.vh) {
-        uint8_t o[16];
+        alignas(16) uint8_t o[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             int i = row * HT + seg + k;
@@ -219,8 +226,9 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
             o[k] = out;
         }
         const int Y = g.y0 + row;
-        if (seg + 16 <= g.vw && ((((size_t)Y * W + g.x0 + seg) & 15) == 0)) {
-            *reinterpret_cast<uint4*>(frame + (size_t)Y * W + g.x0 + seg) = *reinterpret_cast<uint4*>(o);
+        uint8_t* dst = frame + (size_t)Y * W + g.x0 + seg;
+        if (seg + 16 <= g.vw && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(o);
         } else {
             for (int k = 0; k < 16; ++k)
                 if (seg + k < g.vw) frame[(size_t)Y * W + g.x0 + seg + k] = o[k];
