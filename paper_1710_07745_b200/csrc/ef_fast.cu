@@ -170,6 +170,12 @@ k1_classify_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, u
 
 cudaError_t launch_k1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                       uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
+    if (k1v2_supported(P, g)) return launch_k1v2(src, batch, g, P, labels, fix_list, hdr, st);
+    return launch_k1v1(src, batch, g, P, labels, fix_list, hdr, st);
+}
+
+cudaError_t launch_k1v1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
+                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
     size_t smem = k1_smem_bytes(P.r);
     cudaError_t e = cudaFuncSetAttribute(k1_classify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

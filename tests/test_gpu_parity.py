@@ -96,7 +96,8 @@ def test_fast_path_random_vs_oracle(canny, r):
     rng = np.random.default_rng(100 + r)
     sigma = max(0.3, r / 3.0)
     w = O.gaussian_weights(sigma, radius=r)
-    shapes = [(1, 1), (1, 37), (29, 1), (2, 3), (31, 65), (64, 64), (97, 130), (200, 333)]
+    shapes = [(1, 1), (1, 37), (29, 1), (2, 3), (31, 65), (64, 64), (97, 130), (200, 333),
+              (1, 4), (3, 8), (5, 128), (7, 120), (66, 124), (130, 244), (67, 500), (129, 1024)]
     for (h, wd) in shapes:
         for kind in ("noise", "blocks", "ramp"):
             img = _random_image(rng, h, wd, kind)
