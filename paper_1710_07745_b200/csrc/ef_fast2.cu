@@ -36,7 +36,7 @@ constexpr int V2_TH = 64;
 constexpr int V2_BROWS = V2_TH + 4;
 constexpr int V2_ROWS_PER_WARP = V2_TH / V2_WARPS;
 constexpr int MRING = 8;
-constexpr int QCAP = 64;
+constexpr int QCAP = 128;
 
 struct V2Smem {
     float b[V2_BROWS][V2_COLS];
@@ -56,12 +56,17 @@ __device__ __forceinline__ float u8f(uint32_t w, int k) {
     return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | (unsigned)k)) - 8388608.0f;
 }
 
-__device__ __forceinline__ uint32_t load4(const uint8_t* rowp, int c, int W) {
-    if (c >= 0 && c + 3 < W) return __ldg(reinterpret_cast<const unsigned int*>(rowp + c));
+// Lanes whose 4 columns straddle the frame edge gather clamped bytes; kept
+// out of line so the interior path is a single 4-byte load.
+__device__ __noinline__ uint32_t load4_edge(const uint8_t* rowp, int c, int W) {
     uint32_t w = 0;
-#pragma unroll
     for (int k = 0; k < 4; ++k) w |= (uint32_t)rowp[clampi(c + k, 0, W - 1)] << (8 * k);
     return w;
+}
+
+__device__ __forceinline__ uint32_t load4(const uint8_t* rowp, int c, int W, bool col_ok) {
+    if (col_ok) return __ldg(reinterpret_cast<const unsigned int*>(rowp + c));
+    return load4_edge(rowp, c, W);
 }
 
 __device__ __forceinline__ float sqrt_apx(float x) {
@@ -109,11 +114,11 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
     const int c = xv0 + 4 * lane;
     const int W = g.W;
     const bool edge = xv0 < 0 || xv0 + V2_COLS > W;
-    const int rlo = g.g0, rhi = g.g0 + g.H - 1;
-    auto rowp = [&](int Y) {
-        int Yc = clampi(clampi(Y, 0, g.full_H - 1), rlo, rhi);
-        return img + (size_t)(Yc - g.g0) * W;
-    };
+    const bool col_ok = c >= 0 && c + 3 < W;
+    // rows clamp to the frame and to the rows present in the buffer
+    const int rlo = max(0, g.g0), rhi = min(g.full_H - 1, g.g0 + g.H - 1);
+    const uint8_t* base = img - (ptrdiff_t)g.g0 * W;
+    auto rowp = [&](int Y) { return base + min(max(Y, rlo), rhi) * W; };
     float wf[R + 1];
 #pragma unroll
     for (int k = 0; k <= R; ++k) wf[k] = P.wf[k];
@@ -123,12 +128,12 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
     // input row ii (0-based) is global row ys - R + ii
 #pragma unroll
     for (int ii = 0; ii < 2 * R; ++ii) {
-        uint32_t w = load4(rowp(ys - R + ii), c, W);
+        uint32_t w = load4(rowp(ys - R + ii), c, W, col_ok);
 #pragma unroll
         for (int k = 0; k < 4; ++k) p[ii][k] = u8f(w, k);
     }
 #pragma unroll
-    for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = load4(rowp(ys - R + ii), c, W);
+    for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = load4(rowp(ys - R + ii), c, W, col_ok);
 
     for (int u0 = 0; u0 < n; u0 += NR) {
 #pragma unroll
@@ -139,7 +144,7 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
                 const uint32_t w = raw[(s + 2 * R) % NR];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) p[(s + 2 * R) % NR][k] = u8f(w, k);
-                raw[(s + 4 * R) % NR] = load4(rowp(ys - R + u + 4 * R), c, W);
+                raw[(s + 4 * R) % NR] = load4(rowp(ys - R + u + 4 * R), c, W, col_ok);
             }
             float v[4];
 #pragma unroll
@@ -250,18 +255,24 @@ __device__ __forceinline__ void v2_classify_group(const FrameGeom& g, int xv0, i
 template <int R>
 __device__ __forceinline__ void v2_flush(const FrameGeom& g, int xv0, int y0, int& qn, const FastParams& P,
                                          V2Smem& S, int warp, int lane, const V2Out& O) {
-    const int take = min(qn, 32);
-    if (lane < take) {
-        const int e = S.q[warp][lane];
-        v2_classify_group<R>(g, xv0, y0, y0 + (e >> 8), e & 255, P, S, warp, O);
+    // every queued group is classified; at most QCAP - 32 stay behind
+    while (qn > 0) {
+        const int take = min(qn, 32);
+        if (lane < take) {
+            const int e = S.q[warp][lane];
+            v2_classify_group<R>(g, xv0, y0, y0 + (e >> 8), e & 255, P, S, warp, O);
+        }
+        const int rest = qn - take;
+        int moved[QCAP / 32 - 1];
+#pragma unroll
+        for (int j = 0; j < QCAP / 32 - 1; ++j) moved[j] = (lane + 32 * j < rest) ? S.q[warp][32 + lane + 32 * j] : 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < QCAP / 32 - 1; ++j)
+            if (lane + 32 * j < rest) S.q[warp][lane + 32 * j] = moved[j];
+        __syncwarp();
+        qn = rest;
     }
-    const int rest = qn - take;
-    int moved = 0;
-    if (lane < rest) moved = S.q[warp][32 + lane];
-    __syncwarp();
-    if (lane < rest) S.q[warp][lane] = moved;
-    __syncwarp();
-    qn = rest;
 }
 
 template <int R>
@@ -280,11 +291,13 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
     const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
     const float lo_lo = P.lo_lo;
+    // label row pointer of the row being classified (advances one row per step)
+    uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (unsigned long long)(Ys - g.out0) * W + c);
+    const int Wq = W >> 2;
 
     float d[3][4], s[3][4], mr[3][4];
-    int qn = 0, qold = 0;
+    int qn = 0, qprev = 0;
     const int l = 4 * lane;
-    const int ll = max(l - 1, 0), lr = min(l + 4, V2_COLS - 1);
     // b rows jb = Ys-2 .. Ye+1 ; step index t = jb - (Ys-2)
     const int nsteps = Ye - Ys + 4;
     for (int t0 = 0; t0 < nsteps; t0 += 3) {
@@ -295,7 +308,10 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
             const int jb = Ys - 2 + t;
             const float* brow = S.b[clampi(jb, 0, FH - 1) - (y0 - 2)];
             const float4 bb = *reinterpret_cast<const float4*>(brow + l);
-            const float bl = brow[ll], br = brow[lr];
+            // neighbour lanes' edge columns (lane 0 / 31 get their own values:
+            // only columns no output depends on are affected)
+            const float bl = __shfl_up_sync(0xffffffffu, bb.w, 1);
+            const float br = __shfl_down_sync(0xffffffffu, bb.x, 1);
             d[ph][0] = bb.y - bl;
             d[ph][1] = bb.z - bb.x;
             d[ph][2] = bb.w - bb.y;
@@ -326,35 +342,30 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
                 }
             }
             if (t >= 4) {
-                // classify row Yc = jb - 2 (its magnitudes were produced one step ago)
+                // row Yc = jb - 2: its magnitudes were produced one step ago
                 const int Yc = jb - 2;
-                __syncwarp();
                 const int pp = (ph + 2) % 3;
                 bool cand = false;
                 if (out_lane) {
-                    cand = mr[pp][0] >= lo_lo || mr[pp][1] >= lo_lo || mr[pp][2] >= lo_lo || mr[pp][3] >= lo_lo;
-                    if (!cand)
-                        *reinterpret_cast<uint32_t*>(O.labels + O.out_base + (unsigned long long)(Yc - g.out0) * W + c) = fill;
+                    cand = fmaxf(fmaxf(mr[pp][0], mr[pp][1]), fmaxf(mr[pp][2], mr[pp][3])) >= lo_lo;
+                    if (!cand) *lab = fill;
                 }
+                lab += Wq;
                 const unsigned ballot = __ballot_sync(0xffffffffu, cand);
-                if (ballot) {
-                    if (cand) {
-                        const int pos = qn + __popc(ballot & ((1u << lane) - 1u));
-                        S.q[warp][pos] = ((Yc - y0) << 8) | lane;
-                    }
-                    if (qn == 0) qold = Yc;
-                    qn += __popc(ballot);
-                }
-                __syncwarp();
-                if (qn >= 32 || (qn > 0 && Yc >= qold + 4)) {  // ring slot of qold-1 is reused at jb = qold+7
-                    v2_flush<R>(g, xv0, y0, qn, P, S, warp, lane, O);
-                    if (qn > 0) qold = y0 + (S.q[warp][0] >> 8);
-                }
+                if (cand) S.q[warp][qn + __popc(ballot & ((1u << lane) - 1u))] = ((Yc - y0) << 8) | lane;
+                qn += __popc(ballot);
             }
         }
+        // classify queued groups when 32 are waiting, when entries have already
+        // waited one 3-step group (an entry for row Yc needs ring rows Yc-1..Yc+1;
+        // the 8-row ring reuses the slot of Yc-1 at step jb = Yc+8, and two
+        // groups after its enqueue step jb = Yc+2 is at most jb = Yc+7), or at the end
+        if (qn >= 32 || qprev > 0 || t0 + 3 >= nsteps) {
+            __syncwarp();
+            v2_flush<R>(g, xv0, y0, qn, P, S, warp, lane, O);
+        }
+        qprev = qn;
     }
-    __syncwarp();
-    while (qn > 0) v2_flush<R>(g, xv0, y0, qn, P, S, warp, lane, O);
 }
 
 template <int R>

@@ -31,12 +31,14 @@ constexpr int H_THREADS = 256;  // 16 pixels per thread
 constexpr int NO_POS = 0x7fffffff;
 
 struct TileCCL {
-    int par[HT * HT];
-    int minpos[HT * HT];
-    uint8_t lab[HT * HT];
-    uint8_t sflag[HT * HT];
+    unsigned long long fgrow[HT];  // foreground (label != 0) bit per pixel, one word per row
+    unsigned long long strow[HT];  // strong bit per pixel
+    int par[HT * HT];              // union-find parent; initialised for foreground pixels only
+    int minpos[HT * HT];           // smallest perimeter slot per root (foreground only)
+    unsigned char sflag[HT * HT];  // component holds a strong pixel (per root)
     int pending;
     int nodes;
+    int any;
 };
 
 __device__ __forceinline__ int sfind(int* par, int i) {
@@ -124,79 +126,132 @@ __device__ __forceinline__ void slot_pixel(int s, int vh, int vw, int& y, int& x
     else { y = s - 192; x = vw - 1; }
 }
 
-// Shared tile CCL used by H1 and H4.  After return (and a barrier) par[] holds
-// roots for every foreground pixel, sflag[root] marks strong components and
-// minpos[root] the smallest perimeter slot (NO_POS if interior).
-__device__ void tile_ccl(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g,
-                         TileCCL& s) {
+// Pack the foreground / strong bits of 4 label bytes (values 0/1/2) into nibbles.
+__device__ __forceinline__ void pack4(uint32_t w, uint32_t& fg, uint32_t& st) {
+    const uint32_t nz = (w | (w >> 1)) & 0x01010101u;
+    const uint32_t sg = (w >> 1) & 0x01010101u;
+    fg = (nz * 0x10204080u) >> 28;
+    st = (sg * 0x10204080u) >> 28;
+}
+
+// Shared tile CCL used by H1 and H4.  Work is proportional to the foreground:
+// label bytes become per-row bit masks, union-find runs over foreground pixels
+// only.  After return (and a barrier) par[] holds roots for every foreground
+// pixel, sflag[root] marks strong components and minpos[root] the smallest
+// perimeter slot (NO_POS if interior).  Returns this thread's 16-bit
+// foreground mask (row = tid/4, columns 16*(tid%4) ..).
+__device__ uint32_t tile_ccl(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g, TileCCL& s) {
     const int tid = threadIdx.x;
     const int row = tid >> 2, seg = (tid & 3) * 16;
     const uint8_t* frame = labels + (size_t)g.f * H * W;
     const int Y = g.y0 + row;
-    uint8_t v[16];
+    uint32_t words[4] = {0u, 0u, 0u, 0u};
     const uint8_t* src = frame + (size_t)Y * W + g.x0 + seg;
     if (row < g.vh && seg + 16 <= g.vw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        uint4 q = *reinterpret_cast<const uint4*>(src);
-        const uint8_t* qb = reinterpret_cast<const uint8_t*>(&q);
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
+        words[0] = q.x; words[1] = q.y; words[2] = q.z; words[3] = q.w;
+    } else if (row < g.vh) {
+        for (int k = 0; k < 16; ++k)
+            if (seg + k < g.vw) words[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
+    }
+    uint32_t fg = 0, st = 0;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = qb[k];
-    } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            int X = seg + k;
-            v[k] = (row < g.vh && X < g.vw) ? frame[(size_t)Y * W + g.x0 + X] : 0;
+    for (int j = 0; j < 4; ++j) {
+        uint32_t f, t;
+        pack4(words[j], f, t);
+        fg |= f << (4 * j);
+        st |= t << (4 * j);
+    }
+    if (tid == 0) s.any = 0;
+    // segment masks -> row words (4 threads per row, 16 bits each)
+    reinterpret_cast<unsigned short*>(&s.fgrow[row])[tid & 3] = (unsigned short)fg;
+    reinterpret_cast<unsigned short*>(&s.strow[row])[tid & 3] = (unsigned short)st;
+    // init only foreground pixels; runs inside the segment pre-linked to their start
+    {
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const int i = row * HT + seg + k;
+            const bool left_in_run = k > 0 && ((fg >> (k - 1)) & 1u);
+            int start = k;
+            if (left_in_run) {  // start of the run containing k inside this segment
+                const uint32_t below = ~fg & ((1u << k) - 1u);
+                start = below ? (32 - __clz(below)) : 0;
+            }
+            s.par[i] = row * HT + seg + start;
+            s.minpos[i] = NO_POS;
+            s.sflag[i] = 0;
         }
     }
-    int run = -1;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        int i = row * HT + seg + k;
-        s.lab[i] = v[k];
-        s.sflag[i] = 0;
-        s.minpos[i] = NO_POS;
-        if (v[k]) {
-            if (run < 0) run = i;
-            s.par[i] = run;  // pre-link runs inside this thread's segment
-        } else {
-            run = -1;
-            s.par[i] = i;
-        }
-    }
-    __syncthreads();
-    // unions with W (across segments only), NW, N, NE
-#pragma unroll 1
-    for (int k = 0; k < 16; ++k) {
-        int x = seg + k, i = row * HT + x;
-        if (!v[k]) continue;
-        if (k == 0 && x > 0 && s.lab[i - 1]) sunite(s.par, i, i - 1);
-        if (row > 0) {
-            int up = i - HT;
-            if (s.lab[up]) sunite(s.par, i, up);
-            else {
-                if (x > 0 && s.lab[up - 1]) sunite(s.par, i, up - 1);
-                if (x < HT - 1 && s.lab[up + 1]) sunite(s.par, i, up + 1);
+    const int any = __syncthreads_or(fg != 0);
+    if (!any) return 0;
+    // unions: W across segments, N / NW / NE from the row above (bit tests)
+    const unsigned long long up = row > 0 ? s.fgrow[row - 1] : 0ull;
+    const unsigned long long cur = s.fgrow[row];
+    {
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const int x = seg + k, i = row * HT + x;
+            if (k == 0 && x > 0 && ((cur >> (x - 1)) & 1ull)) sunite(s.par, i, i - 1);
+            if (up) {
+                if ((up >> x) & 1ull) {
+                    sunite(s.par, i, i - HT);
+                } else {
+                    if (x > 0 && ((up >> (x - 1)) & 1ull)) sunite(s.par, i, i - HT - 1);
+                    if (x < HT - 1 && ((up >> (x + 1)) & 1ull)) sunite(s.par, i, i - HT + 1);
+                }
             }
         }
     }
     __syncthreads();
-    // roots, strong flags, perimeter minima.  Roots go to registers first:
-    // concurrent path-halving writes could otherwise overwrite a stored root
-    // with a non-root ancestor; the forest is only rewritten after a barrier.
+    // roots into registers first (concurrent path halving may rewrite par[])
     int roots[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        int x = seg + k, i = row * HT + x;
-        roots[k] = v[k] ? sfind(s.par, i) : -1;
-        if (!v[k]) continue;
-        if (v[k] == kStrong) s.sflag[roots[k]] = 1;
-        int p = perim_slot(row, x, g.vh, g.vw);
-        if (p != NO_POS) atomicMin(&s.minpos[roots[k]], p);
+    {
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const int x = seg + k, i = row * HT + x;
+            const int r = sfind(s.par, i);
+            roots[k] = r;
+            if ((st >> k) & 1u) s.sflag[r] = 1;
+            const int p = perim_slot(row, x, g.vh, g.vw);
+            if (p != NO_POS) atomicMin(&s.minpos[r], p);
+        }
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-        if (v[k]) s.par[row * HT + seg + k] = roots[k];
+    {
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            s.par[row * HT + seg + k] = roots[k];
+        }
+    }
     __syncthreads();
+    return fg;
+}
+
+// 16 bits -> 16 bytes (0/1)
+__device__ __forceinline__ uint4 expand16(uint32_t bits) {
+    uint4 o;
+    o.x = ((bits & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.y = (((bits >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.z = (((bits >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+    o.w = (((bits >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return o;
+}
+
+__device__ __forceinline__ void store16(uint8_t* dst, int valid, uint4 o) {
+    if (valid >= 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<uint4*>(dst) = o;
+    } else {
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        for (int k = 0; k < valid && k < 16; ++k) dst[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+    }
 }
 
 __global__ void __launch_bounds__(H_THREADS)
@@ -207,51 +262,38 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
     const long long tile = blockIdx.x;
     TileGeo g = tile_geo(tile, H, W, tiles_x, tiles_y);
     if (threadIdx.x == 0) { s.pending = 0; s.nodes = 0; }
-    tile_ccl(labels, H, W, g, s);
+    const uint32_t fg = tile_ccl(labels, H, W, g, s);
     const int tid = threadIdx.x;
     const int row = tid >> 2, seg = (tid & 3) * 16;
-    uint8_t* frame = final_out + (size_t)g.f * H * W;
+    uint32_t fin = 0;
     bool pend = false;
-    if (row < g.vh) {
-        alignas(16) uint8_t o[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            int i = row * HT + seg + k;
-            uint8_t out = 0;
-            if (s.lab[i]) {
-                int root = s.par[i];
-                if (s.sflag[root]) out = 1;
-                else if (s.minpos[root] != NO_POS) pend = true;
-            }
-            o[k] = out;
-        }
-        const int Y = g.y0 + row;
-        uint8_t* dst = frame + (size_t)Y * W + g.x0 + seg;
-        if (seg + 16 <= g.vw && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(o);
-        } else {
-            for (int k = 0; k < 16; ++k)
-                if (seg + k < g.vw) frame[(size_t)Y * W + g.x0 + seg + k] = o[k];
+    {
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const int root = s.par[row * HT + seg + k];
+            if (s.sflag[root]) fin |= 1u << k;
+            else if (s.minpos[root] != NO_POS) pend = true;
         }
     }
+    if (row < g.vh && seg < g.vw)
+        store16(final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg, g.vw - seg, expand16(fin));
     if (pend) s.pending = 1;
-    // perimeter slots: node id of the component at each slot, -1 if background
+    // perimeter slot tid: node id of the component at that slot, -1 if background
     {
-        int p = tid;  // H_THREADS == HP
+        const int p = tid;  // H_THREADS == HP
         int y, x;
         slot_pixel(p, g.vh, g.vw, y, x);
         int node = -1;
-        bool valid = (p < 64 || (p >= 64 && p < 128)) ? (x < g.vw) : (y < g.vh);
-        if (valid) {
-            int i = y * HT + x;
-            if (s.lab[i]) {
-                int root = s.par[i];
-                node = (int)(tile * HP) + s.minpos[root];
-                if (s.minpos[root] == p) {
-                    gpar[node] = node;
-                    gstrong[node] = s.sflag[root];
-                    atomicAdd(&s.nodes, 1);
-                }
+        const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
+        if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
+            const int root = s.par[y * HT + x];
+            node = (int)(tile * HP) + s.minpos[root];
+            if (s.minpos[root] == p) {
+                gpar[node] = node;
+                gstrong[node] = s.sflag[root];
+                atomicAdd(&s.nodes, 1);
             }
         }
         perim[tile * HP + p] = node;
@@ -336,21 +378,18 @@ hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
     const long long tile = blockIdx.x;
     if (!pending[tile]) return;
     TileGeo g = tile_geo(tile, H, W, tiles_x, tiles_y);
-    tile_ccl(labels, H, W, g, s);
+    const uint32_t fg = tile_ccl(labels, H, W, g, s);
     const int tid = threadIdx.x;
     const int row = tid >> 2, seg = (tid & 3) * 16;
-    if (row >= g.vh) return;
-    uint8_t* frame = final_out + (size_t)g.f * H * W;
-    const int Y = g.y0 + row;
-    for (int k = 0; k < 16; ++k) {
-        int x = seg + k;
-        if (x >= g.vw) break;
-        int i = row * HT + x;
-        if (!s.lab[i]) continue;
-        int root = s.par[i];
+    uint32_t m = fg;
+    uint8_t* out = final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const int root = s.par[row * HT + seg + k];
         if (s.sflag[root] || s.minpos[root] == NO_POS) continue;
-        int node = (int)(tile * HP) + s.minpos[root];
-        if (gstrong[gfind_ro(gpar, node)]) frame[(size_t)Y * W + g.x0 + x] = 1;
+        const int node = (int)(tile * HP) + s.minpos[root];
+        if (gstrong[gfind_ro(gpar, node)]) out[k] = 1;
     }
 }
 
