@@ -100,86 +100,113 @@ __device__ __forceinline__ void edge_fix(float (&v)[4], int xv0, int lane, int W
 }
 
 // ---------------------------------------------------------------- phase 1 --
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// Rows of b computed per warp in phase 1: the tile's 68 b rows split 4 ways.
+constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 17
+
 template <int R>
 __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const FrameGeom& g, int xv0, int y0,
                                           const FastParams& P, V2Smem& S, int warp, int lane) {
     constexpr int NR = V2Cfg<R>::NR;
-    const int bg0 = max(y0 - 2, 0);
-    const int bg1 = min(y0 + V2_TH + 2, g.full_H);
-    const int nrows = bg1 - bg0;
-    const int per = (nrows + V2_WARPS - 1) / V2_WARPS;
-    const int ys = bg0 + warp * per;
-    const int n = min(per, bg1 - ys);
-    if (n <= 0) return;
     const int c = xv0 + 4 * lane;
     const int W = g.W;
     const bool edge = xv0 < 0 || xv0 + V2_COLS > W;
     const bool col_ok = c >= 0 && c + 3 < W;
-    // rows clamp to the frame and to the rows present in the buffer
+    // b rows of this warp: global ys .. ys+16 (a fixed trip count keeps the
+    // warp converged; rows outside the frame are computed from clamped input
+    // and simply not stored)
+    const int ys = y0 - 2 + warp * V2_P1_ROWS;
+    const int vlo = max(ys, max(y0 - 2, 0));
+    const int vhi = min(ys + V2_P1_ROWS, min(y0 + V2_TH + 2, g.full_H));
+    // input rows clamp to the frame and to the rows present in the buffer
     const int rlo = max(0, g.g0), rhi = min(g.full_H - 1, g.g0 + g.H - 1);
     const uint8_t* base = img - (ptrdiff_t)g.g0 * W;
-    auto rowp = [&](int Y) { return base + min(max(Y, rlo), rhi) * W; };
-    float wf[R + 1];
+    const bool rclamp = ys - R < rlo || ys + V2_P1_ROWS + 3 * R > rhi;  // warp-uniform
+    auto rowp = [&](int Y) { return base + (ptrdiff_t)(rclamp ? min(max(Y, rlo), rhi) : Y) * W; };
+    float2 wf2[R + 1];
 #pragma unroll
-    for (int k = 0; k <= R; ++k) wf[k] = P.wf[k];
+    for (int k = 0; k <= R; ++k) wf2[k] = f2(P.wf[k], P.wf[k]);
+    const float2 magic = f2(8388608.0f, 8388608.0f);
+    auto cvt = [&](uint32_t w, float2& lo, float2& hi) {
+        lo = add2(f2(__int_as_float(__byte_perm(w, 0x4B000000u, 0x7540u)),
+                     __int_as_float(__byte_perm(w, 0x4B000000u, 0x7541u))), f2(-magic.x, -magic.y));
+        hi = add2(f2(__int_as_float(__byte_perm(w, 0x4B000000u, 0x7542u)),
+                     __int_as_float(__byte_perm(w, 0x4B000000u, 0x7543u))), f2(-magic.x, -magic.y));
+    };
 
-    float p[NR][4];
+    float2 p[NR][2];  // converted input rows: columns (c, c+1), (c+2, c+3)
     uint32_t raw[NR];
-    // input row ii (0-based) is global row ys - R + ii
+    // input row ii is global row ys - R + ii
 #pragma unroll
-    for (int ii = 0; ii < 2 * R; ++ii) {
-        uint32_t w = load4(rowp(ys - R + ii), c, W, col_ok);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) p[ii][k] = u8f(w, k);
-    }
+    for (int ii = 0; ii < 2 * R; ++ii) cvt(load4(rowp(ys - R + ii), c, W, col_ok), p[ii][0], p[ii][1]);
 #pragma unroll
     for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = load4(rowp(ys - R + ii), c, W, col_ok);
+    float* out = &S.b[ys - (y0 - 2)][4 * lane];
 
-    for (int u0 = 0; u0 < n; u0 += NR) {
 #pragma unroll
-        for (int s = 0; s < NR; ++s) {
-            const int u = u0 + s;
-            if (u >= n) break;
-            {   // newest input row ii = u + 2R, prefetch ii = u + 4R
-                const uint32_t w = raw[(s + 2 * R) % NR];
+    for (int u = 0; u < V2_P1_ROWS; ++u) {
+        const int s = u % NR;
+        cvt(raw[(s + 2 * R) % NR], p[(s + 2 * R) % NR][0], p[(s + 2 * R) % NR][1]);
+        if (u + 2 * R < V2_P1_ROWS) raw[(s + 4 * R) % NR] = load4(rowp(ys - R + u + 4 * R), c, W, col_ok);
+        // vertical pass on column pairs
+        float2 v01 = mul2(wf2[0], p[(s + R) % NR][0]);
+        float2 v23 = mul2(wf2[0], p[(s + R) % NR][1]);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) p[(s + 2 * R) % NR][k] = u8f(w, k);
-                raw[(s + 4 * R) % NR] = load4(rowp(ys - R + u + 4 * R), c, W, col_ok);
-            }
-            float v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float acc = wf[0] * p[(s + R) % NR][k];
-#pragma unroll
-                for (int o = 1; o <= R; ++o)
-                    acc = fmaf(wf[o], p[(s + R - o) % NR][k] + p[(s + R + o) % NR][k], acc);
-                v[k] = acc;
-            }
-            // columns c-R .. c+3+R: e[j] is column c - R + j
-            float e[4 + 2 * R];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) e[R + k] = v[k];
-#pragma unroll
-            for (int o = 1; o <= R; ++o) {
-                e[R - o] = __shfl_up_sync(0xffffffffu, v[4 - o], 1);
-                e[R + 3 + o] = __shfl_down_sync(0xffffffffu, v[o - 1], 1);
-            }
-            float b[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float acc = wf[0] * e[R + k];
-#pragma unroll
-                for (int o = 1; o <= R; ++o) acc = fmaf(wf[o], e[R + k - o] + e[R + k + o], acc);
-                b[k] = acc;
-            }
-            if (edge) edge_fix(b, xv0, lane, W);
-            const int lr = ys + u - (y0 - 2);
-            *reinterpret_cast<float4*>(&S.b[lr][4 * lane]) = make_float4(b[0], b[1], b[2], b[3]);
+        for (int o = 1; o <= R; ++o) {
+            v01 = fma2(wf2[o], add2(p[(s + R - o) % NR][0], p[(s + R + o) % NR][0]), v01);
+            v23 = fma2(wf2[o], add2(p[(s + R - o) % NR][1], p[(s + R + o) % NR][1]), v23);
         }
+        // horizontal pass: neighbours' pairs by 64-bit shuffles
+        // e[j] = column c - 4 + j, j = 0..11 (lane-1's 4, own 4, lane+1's 4)
+        float e[12];
+        {
+            const double d01 = __hiloint2double(__float_as_int(v01.y), __float_as_int(v01.x));
+            const double d23 = __hiloint2double(__float_as_int(v23.y), __float_as_int(v23.x));
+            const double l23 = __shfl_up_sync(0xffffffffu, d23, 1);
+            const double r01 = __shfl_down_sync(0xffffffffu, d01, 1);
+            const double l01 = R > 2 ? __shfl_up_sync(0xffffffffu, d01, 1) : 0.0;
+            const double r23 = R > 2 ? __shfl_down_sync(0xffffffffu, d23, 1) : 0.0;
+            e[0] = __int_as_float(__double2loint(l01)); e[1] = __int_as_float(__double2hiint(l01));
+            e[2] = __int_as_float(__double2loint(l23)); e[3] = __int_as_float(__double2hiint(l23));
+            e[4] = v01.x; e[5] = v01.y; e[6] = v23.x; e[7] = v23.y;
+            e[8] = __int_as_float(__double2loint(r01)); e[9] = __int_as_float(__double2hiint(r01));
+            e[10] = __int_as_float(__double2loint(r23)); e[11] = __int_as_float(__double2hiint(r23));
+        }
+        // b(k) = w0 e[4+k] + sum_o w_o (e[4+k-o] + e[4+k+o]); even o on aligned pairs
+        float2 b01 = mul2(wf2[0], f2(e[4], e[5]));
+        float2 b23 = mul2(wf2[0], f2(e[6], e[7]));
+#pragma unroll
+        for (int o = 1; o <= R; ++o) {
+            if ((o & 1) == 0) {
+                b01 = fma2(wf2[o], add2(f2(e[4 - o], e[5 - o]), f2(e[4 + o], e[5 + o])), b01);
+                b23 = fma2(wf2[o], add2(f2(e[6 - o], e[7 - o]), f2(e[6 + o], e[7 + o])), b23);
+            } else {
+                b01.x = fmaf(wf2[o].x, e[4 - o] + e[4 + o], b01.x);
+                b01.y = fmaf(wf2[o].x, e[5 - o] + e[5 + o], b01.y);
+                b23.x = fmaf(wf2[o].x, e[6 - o] + e[6 + o], b23.x);
+                b23.y = fmaf(wf2[o].x, e[7 - o] + e[7 + o], b23.y);
+            }
+        }
+        float b[4] = {b01.x, b01.y, b23.x, b23.y};
+        if (edge) edge_fix(b, xv0, lane, W);
+        const int Y = ys + u;
+        if (Y >= vlo && Y < vhi) *reinterpret_cast<float4*>(out) = make_float4(b[0], b[1], b[2], b[3]);
+        out += V2_COLS;
     }
 }
 
 // ---------------------------------------------------------------- phase 2 --
+// The few scalars the out-of-line classifier needs (kept in registers).
+struct V2Cls {
+    float lo_lo, lo_hi, hi_lo, hi_hi, e_nms, e_sec;
+    int cls0;
+    int W, FH, out0;
+};
+
 struct V2Out {
     uint8_t* labels;
     unsigned long long out_base;
@@ -191,9 +218,9 @@ __device__ __forceinline__ int mslot(int Y) { return (Y + MRING) & (MRING - 1); 
 
 // Classify the 4 pixels of one queued group (certified; kFlag otherwise).
 template <int R>
-__device__ __forceinline__ void v2_classify_group(const FrameGeom& g, int xv0, int y0, int Yc, int cl,
-                                                  const FastParams& P, V2Smem& S, int warp, const V2Out& O) {
-    const int W = g.W, FH = g.full_H;
+__device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0, int Yc, int cl, V2Smem& S,
+                                                  int warp, const V2Out O) {
+    const int W = P.W, FH = P.FH;
     const float t1 = 0.41421356237309503f;
     const float* mu = S.m[warp][mslot(Yc - 1)];
     const float* mc = S.m[warp][mslot(Yc)];
@@ -203,11 +230,11 @@ __device__ __forceinline__ void v2_classify_group(const FrameGeom& g, int xv0, i
     const float* bd = S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)];
     uint32_t packed = 0;
     const int cc0 = 4 * cl;
-    const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - g.out0) * W;
+    const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * W;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int cc = cc0 + k;
-        const float c = mc[cc];
+        const float c = sqrt_apx(mc[cc]);
         int cls;
         if (c > P.hi_hi) cls = 2;
         else if (c >= P.hi_lo) cls = -1;
@@ -229,12 +256,12 @@ __device__ __forceinline__ void v2_classify_group(const FrameGeom& g, int xv0, i
             if (fabsf(uu) <= P.e_sec || fabsf(vv) <= P.e_sec) {
                 flag = true;
             } else {
-                float n1, n2;
+                float n1, n2;  // squared magnitudes of the two neighbours along the sector
                 if (uu > 0.f) { n1 = mc[cc - 1]; n2 = mc[cc + 1]; }                       // 0
                 else if (vv > 0.f) { n1 = mu[cc]; n2 = md[cc]; }                          // 90
                 else if ((gx > 0.f) == (gy > 0.f)) { n1 = mu[cc + 1]; n2 = md[cc - 1]; }  // 45
                 else { n1 = mu[cc - 1]; n2 = md[cc + 1]; }                                // 135
-                float d = c - fmaxf(n1, n2);
+                float d = c - sqrt_apx(fmaxf(n1, n2));
                 if (d < -P.e_nms) lab = (uint32_t)P.cls0;
                 else if (d > P.e_nms) lab = (uint32_t)cls;
                 else flag = true;
@@ -253,14 +280,14 @@ __device__ __forceinline__ void v2_classify_group(const FrameGeom& g, int xv0, i
 }
 
 template <int R>
-__device__ __forceinline__ void v2_flush(const FrameGeom& g, int xv0, int y0, int& qn, const FastParams& P,
-                                         V2Smem& S, int warp, int lane, const V2Out& O) {
+__device__ __noinline__ int v2_flush(const V2Cls P, int xv0, int y0, int qn, V2Smem& S, int warp, int lane,
+                                     const V2Out O) {
     // every queued group is classified; at most QCAP - 32 stay behind
     while (qn > 0) {
         const int take = min(qn, 32);
         if (lane < take) {
             const int e = S.q[warp][lane];
-            v2_classify_group<R>(g, xv0, y0, y0 + (e >> 8), e & 255, P, S, warp, O);
+            v2_classify_group<R>(P, xv0, y0, y0 + (e >> 8), e & 255, S, warp, O);
         }
         const int rest = qn - take;
         int moved[QCAP / 32 - 1];
@@ -273,6 +300,7 @@ __device__ __forceinline__ void v2_flush(const FrameGeom& g, int xv0, int y0, in
         __syncwarp();
         qn = rest;
     }
+    return qn;
 }
 
 template <int R>
@@ -280,89 +308,100 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
                                           int warp, int lane, const V2Out& O) {
     constexpr int HXA = V2Cfg<R>::HXA;
     constexpr int OW = V2Cfg<R>::OW;
+    constexpr int NSTEP = V2_ROWS_PER_WARP + 4;  // b rows Y0w-2 .. Y0w+17 (one extra no-op step)
     const int W = g.W, FH = g.full_H;
-    const int oy0 = max(y0, g.out0), oy1 = min(y0 + V2_TH, g.out0 + g.rows);
-    const int Ys = max(y0 + warp * V2_ROWS_PER_WARP, oy0);
-    const int Ye = min(y0 + (warp + 1) * V2_ROWS_PER_WARP, oy1);
-    if (Ys >= Ye) return;
+    const int Y0w = y0 + warp * V2_ROWS_PER_WARP;
+    const int oy0 = max(Y0w, g.out0), oy1 = min(Y0w + V2_ROWS_PER_WARP, g.out0 + g.rows);
     const bool edge = xv0 < 0 || xv0 + V2_COLS > W;
+    const bool vclamp = Y0w - 2 < 0 || Y0w + V2_ROWS_PER_WARP + 1 >= FH;  // warp-uniform
     const int c = xv0 + 4 * lane;
     // output lane: its 4 columns lie inside [x0, x0 + OW) and inside the frame
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
     const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
-    const float lo_lo = P.lo_lo;
-    // label row pointer of the row being classified (advances one row per step)
-    uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (unsigned long long)(Ys - g.out0) * W + c);
+    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, W, FH, g.out0};
+    const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
+    uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(Y0w - g.out0) * W + c);
     const int Wq = W >> 2;
-
-    float d[3][4], s[3][4], mr[3][4];
-    int qn = 0, qprev = 0;
     const int l = 4 * lane;
-    // b rows jb = Ys-2 .. Ye+1 ; step index t = jb - (Ys-2)
-    const int nsteps = Ye - Ys + 4;
-    for (int t0 = 0; t0 < nsteps; t0 += 3) {
+    const float* bp = &S.b[Y0w - 2 - (y0 - 2)][l];
+    float* mring = S.m[warp][0];
+
+    float d[3][4], sm[3][4];
+    float2 mq[3][2];
+    int qn = 0, qprev = 0;
+    constexpr int NGRP = (NSTEP + 2) / 3;  // 7 groups of 3 steps; the 21st step is a no-op row
+#pragma unroll 1
+    for (int grp = 0; grp < NGRP; ++grp) {
 #pragma unroll
         for (int ph = 0; ph < 3; ++ph) {
-            const int t = t0 + ph;
-            if (t >= nsteps) break;
-            const int jb = Ys - 2 + t;
-            const float* brow = S.b[clampi(jb, 0, FH - 1) - (y0 - 2)];
-            const float4 bb = *reinterpret_cast<const float4*>(brow + l);
-            // neighbour lanes' edge columns (lane 0 / 31 get their own values:
-            // only columns no output depends on are affected)
+            const int t = grp * 3 + ph;
+            const int jb = Y0w - 2 + t;
+            const float* brow = vclamp ? &S.b[clampi(jb, 0, FH - 1) - (y0 - 2)][l] : bp;
+            bp += V2_COLS;
+            const float4 bb = *reinterpret_cast<const float4*>(brow);
+            // neighbour lanes' edge columns (lane 0 / 31 get wrapped values: only
+            // columns no output depends on are affected)
             const float bl = __shfl_up_sync(0xffffffffu, bb.w, 1);
             const float br = __shfl_down_sync(0xffffffffu, bb.x, 1);
             d[ph][0] = bb.y - bl;
             d[ph][1] = bb.z - bb.x;
             d[ph][2] = bb.w - bb.y;
             d[ph][3] = br - bb.z;
-            s[ph][0] = fmaf(2.f, bb.x, bl + bb.y);
-            s[ph][1] = fmaf(2.f, bb.y, bb.x + bb.z);
-            s[ph][2] = fmaf(2.f, bb.z, bb.y + bb.w);
-            s[ph][3] = fmaf(2.f, bb.w, bb.z + br);
+            sm[ph][0] = fmaf(2.f, bb.x, bl + bb.y);
+            sm[ph][1] = fmaf(2.f, bb.y, bb.x + bb.z);
+            sm[ph][2] = fmaf(2.f, bb.z, bb.y + bb.w);
+            sm[ph][3] = fmaf(2.f, bb.w, bb.z + br);
+            // squared magnitude of row Ym = jb-1 from b rows jb-2 (pu), jb-1 (pm), jb (ph)
+            // (meaningful from t >= 2; earlier steps store into ring rows no
+            // classification reads before they are rewritten)
+            const int pu = (ph + 1) % 3, pm = (ph + 2) % 3;
+            const float2 two = f2(2.f, 2.f);
+            const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[ph][0], d[ph][1])));
+            const float2 gx23 = fma2(two, f2(d[pm][2], d[pm][3]), add2(f2(d[pu][2], d[pu][3]), f2(d[ph][2], d[ph][3])));
+            const float2 gy01 = add2(f2(sm[ph][0], sm[ph][1]), f2(-sm[pu][0], -sm[pu][1]));
+            const float2 gy23 = add2(f2(sm[ph][2], sm[ph][3]), f2(-sm[pu][2], -sm[pu][3]));
+            float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
+            float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
+            if (edge) {
+                float m4[4] = {m01.x, m01.y, m23.x, m23.y};
+                edge_fix(m4, xv0, lane, W);
+                m01 = f2(m4[0], m4[1]);
+                m23 = f2(m4[2], m4[3]);
+            }
+            mq[ph][0] = m01;
+            mq[ph][1] = m23;
             const int Ym = jb - 1;
+            const float4 mv = make_float4(m01.x, m01.y, m23.x, m23.y);
             if (t >= 2) {
-                // magnitude row Ym from rows jb-2 (ph+1 mod 3), jb-1 (ph+2 mod 3), jb (ph)
-                const int pu = (ph + 1) % 3, pm = (ph + 2) % 3;
-                float m4[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float gx = fmaf(2.f, d[pm][k], d[pu][k] + d[ph][k]);
-                    float gy = s[ph][k] - s[pu][k];
-                    m4[k] = sqrt_apx(fmaf(gx, gx, gy * gy));
-                }
-                if (edge) edge_fix(m4, xv0, lane, W);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) mr[ph][k] = m4[k];
-                if (Ym >= 0 && Ym < FH) {
-                    const float4 mv = make_float4(m4[0], m4[1], m4[2], m4[3]);
-                    *reinterpret_cast<float4*>(&S.m[warp][mslot(Ym)][l]) = mv;
-                    if (Ym == 0) *reinterpret_cast<float4*>(&S.m[warp][mslot(-1)][l]) = mv;
-                    if (Ym == FH - 1) *reinterpret_cast<float4*>(&S.m[warp][mslot(FH)][l]) = mv;
+                if (!vclamp) {
+                    *reinterpret_cast<float4*>(mring + mslot(Ym) * V2_COLS + l) = mv;
+                } else if (Ym >= 0 && Ym < FH) {
+                    *reinterpret_cast<float4*>(mring + mslot(Ym) * V2_COLS + l) = mv;
+                    if (Ym == 0) *reinterpret_cast<float4*>(mring + mslot(-1) * V2_COLS + l) = mv;
+                    if (Ym == FH - 1) *reinterpret_cast<float4*>(mring + mslot(FH) * V2_COLS + l) = mv;
                 }
             }
-            if (t >= 4) {
-                // row Yc = jb - 2: its magnitudes were produced one step ago
-                const int Yc = jb - 2;
-                const int pp = (ph + 2) % 3;
-                bool cand = false;
-                if (out_lane) {
-                    cand = fmaxf(fmaxf(mr[pp][0], mr[pp][1]), fmaxf(mr[pp][2], mr[pp][3])) >= lo_lo;
-                    if (!cand) *lab = fill;
-                }
-                lab += Wq;
-                const unsigned ballot = __ballot_sync(0xffffffffu, cand);
-                if (cand) S.q[warp][qn + __popc(ballot & ((1u << lane) - 1u))] = ((Yc - y0) << 8) | lane;
-                qn += __popc(ballot);
+            // row Yc = jb - 2: its squared magnitudes were produced one step ago
+            const int Yc = jb - 2;
+            const int pp = (ph + 2) % 3;
+            const bool row_ok = t >= 4 && Yc >= oy0 && Yc < oy1;
+            bool cand = false;
+            if (out_lane && row_ok) {
+                cand = fmaxf(fmaxf(mq[pp][0].x, mq[pp][0].y), fmaxf(mq[pp][1].x, mq[pp][1].y)) >= cand_sq;
+                if (!cand) *lab = fill;
             }
+            if (t >= 4) lab += Wq;
+            const unsigned ballot = __ballot_sync(0xffffffffu, cand);
+            if (cand) S.q[warp][qn + __popc(ballot & ((1u << lane) - 1u))] = ((Yc - y0) << 8) | lane;
+            qn += __popc(ballot);
         }
         // classify queued groups when 32 are waiting, when entries have already
         // waited one 3-step group (an entry for row Yc needs ring rows Yc-1..Yc+1;
-        // the 8-row ring reuses the slot of Yc-1 at step jb = Yc+8, and two
-        // groups after its enqueue step jb = Yc+2 is at most jb = Yc+7), or at the end
-        if (qn >= 32 || qprev > 0 || t0 + 3 >= nsteps) {
+        // the 8-row ring reuses the slot of Yc-1 at step jb = Yc+8, and two groups
+        // after its enqueue step jb = Yc+2 is at most jb = Yc+7), or at the end
+        if (qn >= 32 || qprev > 0 || grp == NGRP - 1) {
             __syncwarp();
-            v2_flush<R>(g, xv0, y0, qn, P, S, warp, lane, O);
+            qn = v2_flush<R>(CP, xv0, y0, qn, S, warp, lane, O);
         }
         qprev = qn;
     }
