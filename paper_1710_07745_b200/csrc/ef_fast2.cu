@@ -108,14 +108,14 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 // Rows of b computed per warp in phase 1: the tile's 68 b rows split 4 ways.
 constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 17
 
-template <int R>
+template <int R, bool INTERIOR>
 __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const FrameGeom& g, int xv0, int y0,
                                           const FastParams& P, V2Smem& S, int warp, int lane) {
     constexpr int NR = V2Cfg<R>::NR;
     const int c = xv0 + 4 * lane;
     const int W = g.W;
-    const bool edge = xv0 < 0 || xv0 + V2_COLS > W;
-    const bool col_ok = c >= 0 && c + 3 < W;
+    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
+    const bool col_ok = INTERIOR || (c >= 0 && c + 3 < W);
     // b rows of this warp: global ys .. ys+16 (a fixed trip count keeps the
     // warp converged; rows outside the frame are computed from clamped input
     // and simply not stored)
@@ -125,8 +125,8 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
     // input rows clamp to the frame and to the rows present in the buffer
     const int rlo = max(0, g.g0), rhi = min(g.full_H - 1, g.g0 + g.H - 1);
     const uint8_t* base = img - (ptrdiff_t)g.g0 * W;
-    const bool rclamp = ys - R < rlo || ys + V2_P1_ROWS + 3 * R > rhi;  // warp-uniform
-    auto rowp = [&](int Y) { return base + (ptrdiff_t)(rclamp ? min(max(Y, rlo), rhi) : Y) * W; };
+    // interior tiles never clamp (all input rows exist); 32-bit row offsets
+    auto rowp = [&](int Y) { return base + (INTERIOR ? Y : min(max(Y, rlo), rhi)) * W; };
     float2 wf2[R + 1];
 #pragma unroll
     for (int k = 0; k <= R; ++k) wf2[k] = f2(P.wf[k], P.wf[k]);
@@ -194,7 +194,10 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
         float b[4] = {b01.x, b01.y, b23.x, b23.y};
         if (edge) edge_fix(b, xv0, lane, W);
         const int Y = ys + u;
-        if (Y >= vlo && Y < vhi) *reinterpret_cast<float4*>(out) = make_float4(b[0], b[1], b[2], b[3]);
+        if (INTERIOR || (Y >= vlo && Y < vhi)) {
+            *reinterpret_cast<float2*>(out) = f2(b[0], b[1]);
+            *reinterpret_cast<float2*>(out + 2) = f2(b[2], b[3]);
+        }
         out += V2_COLS;
     }
 }
@@ -303,7 +306,7 @@ __device__ __noinline__ int v2_flush(const V2Cls P, int xv0, int y0, int qn, V2S
     return qn;
 }
 
-template <int R>
+template <int R, bool INTERIOR>
 __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, const FastParams& P, V2Smem& S,
                                           int warp, int lane, const V2Out& O) {
     constexpr int HXA = V2Cfg<R>::HXA;
@@ -312,8 +315,8 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
     const int W = g.W, FH = g.full_H;
     const int Y0w = y0 + warp * V2_ROWS_PER_WARP;
     const int oy0 = max(Y0w, g.out0), oy1 = min(Y0w + V2_ROWS_PER_WARP, g.out0 + g.rows);
-    const bool edge = xv0 < 0 || xv0 + V2_COLS > W;
-    const bool vclamp = Y0w - 2 < 0 || Y0w + V2_ROWS_PER_WARP + 1 >= FH;  // warp-uniform
+    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
+    const bool vclamp = !INTERIOR && (Y0w - 2 < 0 || Y0w + V2_ROWS_PER_WARP + 1 >= FH);
     const int c = xv0 + 4 * lane;
     // output lane: its 4 columns lie inside [x0, x0 + OW) and inside the frame
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
@@ -325,6 +328,7 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
     const int l = 4 * lane;
     const float* bp = &S.b[Y0w - 2 - (y0 - 2)][l];
     float* mring = S.m[warp][0];
+    int mslot_next = mslot(Y0w - 3);  // ring slot of row Ym at step t: mslot(Y0w - 3 + t)
 
     float d[3][4], sm[3][4];
     float2 mq[3][2];
@@ -371,20 +375,26 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
             mq[ph][0] = m01;
             mq[ph][1] = m23;
             const int Ym = jb - 1;
-            const float4 mv = make_float4(m01.x, m01.y, m23.x, m23.y);
+            float* mdst = mring + mslot_next * V2_COLS + l;
+            mslot_next = (mslot_next + 1) & (MRING - 1);
             if (t >= 2) {
-                if (!vclamp) {
-                    *reinterpret_cast<float4*>(mring + mslot(Ym) * V2_COLS + l) = mv;
-                } else if (Ym >= 0 && Ym < FH) {
-                    *reinterpret_cast<float4*>(mring + mslot(Ym) * V2_COLS + l) = mv;
-                    if (Ym == 0) *reinterpret_cast<float4*>(mring + mslot(-1) * V2_COLS + l) = mv;
-                    if (Ym == FH - 1) *reinterpret_cast<float4*>(mring + mslot(FH) * V2_COLS + l) = mv;
+                if (!vclamp || (Ym >= 0 && Ym < FH)) {
+                    *reinterpret_cast<float2*>(mdst) = m01;
+                    *reinterpret_cast<float2*>(mdst + 2) = m23;
+                }
+                if (vclamp && Ym == 0) {
+                    *reinterpret_cast<float2*>(mring + mslot(-1) * V2_COLS + l) = m01;
+                    *reinterpret_cast<float2*>(mring + mslot(-1) * V2_COLS + l + 2) = m23;
+                }
+                if (vclamp && Ym == FH - 1) {
+                    *reinterpret_cast<float2*>(mring + mslot(FH) * V2_COLS + l) = m01;
+                    *reinterpret_cast<float2*>(mring + mslot(FH) * V2_COLS + l + 2) = m23;
                 }
             }
             // row Yc = jb - 2: its squared magnitudes were produced one step ago
             const int Yc = jb - 2;
             const int pp = (ph + 2) % 3;
-            const bool row_ok = t >= 4 && Yc >= oy0 && Yc < oy1;
+            const bool row_ok = t >= 4 && (INTERIOR ? t < NSTEP : (Yc >= oy0 && Yc < oy1));
             bool cand = false;
             if (out_lane && row_ok) {
                 cand = fmaxf(fmaxf(mq[pp][0].x, mq[pp][0].y), fmaxf(mq[pp][1].x, mq[pp][1].y)) >= cand_sq;
@@ -418,10 +428,20 @@ k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     const int xv0 = x0 - V2Cfg<R>::HXA;
     const int y0 = g.out0 + blockIdx.y * V2_TH;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
-    v2_phase1<R>(img, g, xv0, y0, P, S, warp, lane);
-    __syncthreads();
     V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
-    v2_phase2<R>(g, xv0, y0, P, S, warp, lane, O);
+    // interior tile: every column and row of the halo exists in the buffer and
+    // every output row is classified -- no clamps, no predicated stores
+    const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
+                          y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
+    if (interior) {
+        v2_phase1<R, true>(img, g, xv0, y0, P, S, warp, lane);
+        __syncthreads();
+        v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
+    } else {
+        v2_phase1<R, false>(img, g, xv0, y0, P, S, warp, lane);
+        __syncthreads();
+        v2_phase2<R, false>(g, xv0, y0, P, S, warp, lane, O);
+    }
 }
 
 bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 4 && (g.W % 4) == 0; }
