@@ -93,18 +93,21 @@ struct TileGeo {
     int f, tyi, txi, y0, x0, vh, vw;
 };
 
-__device__ __forceinline__ TileGeo tile_geo(long long tile, int H, int W, int tiles_x, int tiles_y) {
+// Tiles are launched on a (tiles_x, tiles_y, frames) grid: no index division.
+__device__ __forceinline__ TileGeo tile_geo_xyz(int txi, int tyi, int f, int H, int W) {
     TileGeo g;
-    long long per = (long long)tiles_x * tiles_y;
-    g.f = (int)(tile / per);
-    int t2 = (int)(tile - (long long)g.f * per);
-    g.tyi = t2 / tiles_x;
-    g.txi = t2 - g.tyi * tiles_x;
+    g.f = f;
+    g.tyi = tyi;
+    g.txi = txi;
     g.y0 = g.tyi * HT;
     g.x0 = g.txi * HT;
     g.vh = min(HT, H - g.y0);
     g.vw = min(HT, W - g.x0);
     return g;
+}
+
+__device__ __forceinline__ long long tile_id_xyz(int tiles_x, int tiles_y) {
+    return ((long long)blockIdx.z * tiles_y + blockIdx.y) * tiles_x + blockIdx.x;
 }
 
 // Perimeter slot(s) of tile-local pixel (y, x) given the valid extent; returns
@@ -259,8 +262,8 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                   uint8_t* __restrict__ final_out, int* __restrict__ perim, int* __restrict__ gpar,
                   uint8_t* __restrict__ gstrong, uint8_t* __restrict__ pending, WsHeader* hdr) {
     __shared__ TileCCL s;
-    const long long tile = blockIdx.x;
-    TileGeo g = tile_geo(tile, H, W, tiles_x, tiles_y);
+    const long long tile = tile_id_xyz(tiles_x, tiles_y);
+    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
     if (threadIdx.x == 0) { s.pending = 0; s.nodes = 0; }
     const uint32_t fg = tile_ccl(labels, H, W, g, s);
     const int tid = threadIdx.x;
@@ -310,8 +313,8 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
 // 64..127 bottom seam columns; thread 0 also does the two corner diagonals.
 __global__ void __launch_bounds__(128)
 hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, const int* __restrict__ perim, int* gpar) {
-    const long long tile = blockIdx.x;
-    TileGeo g = tile_geo(tile, H, W, tiles_x, tiles_y);
+    const long long tile = tile_id_xyz(tiles_x, tiles_y);
+    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
     const int t = threadIdx.x;
     const int* pa = perim + tile * HP;
     if (t < 64) {
@@ -333,7 +336,7 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, const int* __restrict_
             int a = pa[64 + x];
             if (a >= 0) {
                 const int* pc = perim + (tile + tiles_x) * HP;
-                TileGeo gc = tile_geo(tile + tiles_x, H, W, tiles_x, tiles_y);
+                TileGeo gc = tile_geo_xyz(blockIdx.x, blockIdx.y + 1, blockIdx.z, H, W);
                 for (int dx = -1; dx <= 1; ++dx) {
                     int x2 = x + dx;
                     if (x2 < 0 || x2 >= gc.vw) continue;
@@ -375,9 +378,9 @@ hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                   uint8_t* __restrict__ final_out, const int* __restrict__ gpar,
                   const uint8_t* __restrict__ gstrong, const uint8_t* __restrict__ pending) {
     __shared__ TileCCL s;
-    const long long tile = blockIdx.x;
+    const long long tile = tile_id_xyz(tiles_x, tiles_y);
     if (!pending[tile]) return;
-    TileGeo g = tile_geo(tile, H, W, tiles_x, tiles_y);
+    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
     const uint32_t fg = tile_ccl(labels, H, W, g, s);
     const int tid = threadIdx.x;
     const int row = tid >> 2, seg = (tid & 3) * 16;
@@ -436,11 +439,12 @@ HystLayout hyst_layout(int64_t batch, int H, int W) {
 cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    hyst_local_kernel<<<(unsigned)L.tiles, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
+    const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
+    hyst_local_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
                                                                b.perim, b.gpar, b.gstrong, b.pending, hdr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    hyst_merge_kernel<<<(unsigned)L.tiles, 128, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b.perim, b.gpar);
+    hyst_merge_kernel<<<tgrid, 128, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b.perim, b.gpar);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long blocks = (L.slots + 255) / 256;
@@ -452,7 +456,8 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    hyst_final_kernel<<<(unsigned)L.tiles, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
+    const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
+    hyst_final_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
                                                                b.gpar, b.gstrong, b.pending);
     return cudaGetLastError();
 }
