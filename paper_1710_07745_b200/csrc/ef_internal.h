@@ -49,6 +49,9 @@ cudaError_t launch_k1v1(const uint8_t* src, int64_t batch, const FrameGeom& g, c
 cudaError_t launch_k1v2(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                         uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
 bool k1v2_supported(const FastParams& P, const FrameGeom& g);
+cudaError_t launch_k1v4(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
+                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
+bool k1v4_supported(const FastParams& P, const FrameGeom& g);
 
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, int sm_count,
