@@ -238,7 +238,7 @@ __device__ __forceinline__ void v4_warp(const uint8_t* __restrict__ img, const F
     float2 Pg[2][4], q[2][4], s1[2][4], s2[2][4];
     uint32_t* lab32 = reinterpret_cast<uint32_t*>(CP.labels + CP.out_base) + (c >> 2);
     const int Wq = W >> 2;
-    int qn = 0, qage = 0;
+    int qn = 0, qstep = 0;
 
 #pragma unroll 1
     for (int s0 = 0; s0 < STEPS; s0 += PER) {
@@ -297,6 +297,22 @@ __device__ __forceinline__ void v4_warp(const uint8_t* __restrict__ img, const F
             sv[3] = fma2v(two, b[3], add2v(b[2], br));
             const int np = ph ^ 1;
             (void)rs;
+            if (!INTERIOR) {
+                // the reference pads the *blurred* image: b(-1) = b(0), b(FH) = b(FH-1).
+                // In the running Sobel that means d/s(-1) := d/s(0) (fix the
+                // carried state at jb == 0) and d/s(FH) := d/s(FH-1) (at jb == FH).
+                const int jbA = Y0 - 2 + s, jbB = jbA + HB;
+                const bool topA = jbA == 0, topB = jbB == 0, botA = jbA == FH, botB = jbB == FH;
+                if (topA || topB || botA || botB) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (botA) { d[k].x = q[ph][k].x; sv[k].x = s1[ph][k].x; }
+                        if (botB) { d[k].y = q[ph][k].y; sv[k].y = s1[ph][k].y; }
+                        if (topA) { q[ph][k].x = d[k].x; s1[ph][k].x = sv[k].x; }
+                        if (topB) { q[ph][k].y = d[k].y; s1[ph][k].y = sv[k].y; }
+                    }
+                }
+            }
             // row jb-1: gx = P + d, gy = s(jb) - s(jb-2)   (valid from s >= 2)
             float2 m2[4], gxv[4], gyv[4];
 #pragma unroll
@@ -314,8 +330,20 @@ __device__ __forceinline__ void v4_warp(const uint8_t* __restrict__ img, const F
             const int lr = s - 3;
             if (s >= 2) {
                 float2* dst = &S.m[v4slot(lr)][4 * lane];
-                *reinterpret_cast<float4*>(dst) = make_float4(m2[0].x, m2[0].y, m2[1].x, m2[1].y);
-                *reinterpret_cast<float4*>(dst + 2) = make_float4(m2[2].x, m2[2].y, m2[3].x, m2[3].y);
+                const int YAm = Y0 + lr, YBm = YAm + HB;
+                if (INTERIOR || (YAm >= 0 && YAm < FH && YBm >= 0 && YBm < FH)) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(m2[0].x, m2[0].y, m2[1].x, m2[1].y);
+                    *reinterpret_cast<float4*>(dst + 2) = make_float4(m2[2].x, m2[2].y, m2[3].x, m2[3].y);
+                } else {
+                    // rows outside the frame are never stored: rows -1 / FH are
+                    // the aliases written below (row FH's alias lands one step
+                    // before row FH itself would be computed)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (YAm >= 0 && YAm < FH) dst[k].x = m2[k].x;
+                        if (YBm >= 0 && YBm < FH) dst[k].y = m2[k].y;
+                    }
+                }
                 if (!INTERIOR) {
                     // rows -1 / FH alias rows 0 / FH-1 (per strip)
                     const int YA = Y0 + lr, YB = YA + HB;
@@ -337,10 +365,18 @@ __device__ __forceinline__ void v4_warp(const uint8_t* __restrict__ img, const F
                     }
                 }
             }
-            // candidate detection for row lr (A: Y0+lr, B: +HB): groups certainly
-            // below `low` are written now; the rest wait in the queue until the
-            // next row's magnitudes exist
-            const int qready = qn;
+            // 1) queued entries (rows <= lr-1) are complete now that row lr is in
+            //    the ring: classify them when 32 wait, when the oldest is 5 steps
+            //    old (the 8-row ring reuses the slot of its row-1 at age 7), or at
+            //    the end.  Flushing before enqueueing keeps qn <= 31 + 64 < QCAP.
+            __syncwarp();
+            if (qn >= 32 || (qn > 0 && s - qstep >= 5)) {
+                v4_flush(CP, qn, S, lane);
+                __syncwarp();
+                qn = 0;
+            }
+            // 2) candidate detection for row lr (A: Y0+lr, B: +HB): groups
+            //    certainly below `low` are written now, the rest are queued
             if (s >= 3) {
                 const int YA = Y0 + lr, YB = YA + HB;
                 const bool okA = out_lane && lr < HB && (INTERIOR || (YA >= oy0 && YA < oy1));
@@ -367,31 +403,14 @@ __device__ __forceinline__ void v4_warp(const uint8_t* __restrict__ img, const F
                     S.qgy[pos] = make_float4(gyv[0].y, gyv[1].y, gyv[2].y, gyv[3].y);
                 }
                 const int added = __popc(ba) + __popc(bb);
-                if (qready == 0 && added) qage = 0;
+                if (qn == 0 && added) qstep = s;
                 qn += added;
-            }
-            // entries enqueued before this step are complete (their row + 1 is in
-            // the ring).  Flush them when 32 are ready, or when the oldest is 5
-            // steps old (the 8-row ring reuses the slot of its row - 1 at age 7).
-            ++qage;
-            if (qready >= 32 || (qready > 0 && qage >= 5) || s == STEPS - 1) {
-                const int nproc = (s == STEPS - 1) ? qn : qready;
-                __syncwarp();
-                v4_flush(CP, nproc, S, lane);
-                const int rest = qn - nproc;
-                int mv0 = 0, mv1 = 0;
-                float4 g0 = make_float4(0, 0, 0, 0), g1 = g0, h0 = g0, h1 = g0;
-                if (lane < rest) { mv0 = S.qmeta[nproc + lane]; g0 = S.qgx[nproc + lane]; h0 = S.qgy[nproc + lane]; }
-                if (lane + 32 < rest) { mv1 = S.qmeta[nproc + lane + 32]; g1 = S.qgx[nproc + lane + 32]; h1 = S.qgy[nproc + lane + 32]; }
-                __syncwarp();
-                if (lane < rest) { S.qmeta[lane] = mv0; S.qgx[lane] = g0; S.qgy[lane] = h0; }
-                if (lane + 32 < rest) { S.qmeta[lane + 32] = mv1; S.qgx[lane + 32] = g1; S.qgy[lane + 32] = h1; }
-                __syncwarp();
-                qn = rest;
-                qage = 1;  // the moved entries were enqueued this step
             }
         }
     }
+    // entries of the last output row need the final ring row, stored above
+    __syncwarp();
+    if (qn > 0) v4_flush(CP, qn, S, lane);
 }
 
 template <int R>
@@ -411,8 +430,9 @@ k1v4_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     // decided for the whole CTA (block-uniform, so the compiler keeps the
     // warp shuffles convergent): every warp's rows, halo included, exist
     const int Yc0 = g.out0 + blockIdx.y * V4_WARPS * 2 * HB, Yc1 = Yc0 + V4_WARPS * 2 * HB;
+    // (input rows are prefetched 2R rows past the last one used: Yc1 + 1 + 3R)
     const bool interior = xv0 >= 0 && xv0 + V4_COLS <= g.W && Yc0 - 2 - R >= max(g.g0, 0) &&
-                          Yc1 + 2 + R <= min(g.full_H, g.g0 + g.H) && Yc1 <= g.out0 + g.rows;
+                          Yc1 + 2 + 3 * R <= min(g.full_H, g.g0 + g.H) && Yc1 <= g.out0 + g.rows;
     if (interior) v4_warp<R, true>(img, g, P, xv0, Y0, S.w[warp], lane, CP);
     else v4_warp<R, false>(img, g, P, xv0, Y0, S.w[warp], lane, CP);
 }
