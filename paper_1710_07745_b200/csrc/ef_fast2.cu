@@ -32,7 +32,7 @@ namespace ef {
 constexpr int V2_WARPS = 4;
 constexpr int V2_THREADS = 32 * V2_WARPS;
 constexpr int V2_COLS = 128;
-constexpr int V2_TH = 64;
+constexpr int V2_TH = 32;
 constexpr int V2_BROWS = V2_TH + 4;
 constexpr int V2_ROWS_PER_WARP = V2_TH / V2_WARPS;
 constexpr int MRING = 8;
@@ -418,7 +418,7 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
 }
 
 template <int R>
-__global__ void __launch_bounds__(V2_THREADS)
+__global__ void __launch_bounds__(V2_THREADS, 6)
 k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
             unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -451,6 +451,10 @@ static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& 
                             uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
     const int smem = (int)sizeof(V2Smem);
     cudaError_t e = cudaFuncSetAttribute(k1v2_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    // occupancy is shared-memory bound: ask for the largest carveout
+    e = cudaFuncSetAttribute(k1v2_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     dim3 grid((g.W + V2Cfg<R>::OW - 1) / V2Cfg<R>::OW, (g.rows + V2_TH - 1) / V2_TH, (unsigned)batch);
     k1v2_kernel<R><<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr);
