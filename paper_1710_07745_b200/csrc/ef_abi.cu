@@ -56,8 +56,8 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
-    size_t hdr, fix, perim, gpar, gstrong, pending, total;
-    unsigned long long fix_cap;
+    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, total;
+    unsigned long long fix_cap, plist_cap;
     HystLayout hl;
 };
 
@@ -79,6 +79,11 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     off = align_up(off + (size_t)L.hl.slots);
     L.pending = off;
     off = align_up(off + (size_t)L.hl.tiles);
+    L.plist_cap = std::max<unsigned long long>(1ull << 16, npx / 64);
+    L.plist_idx = off;
+    off = align_up(off + L.plist_cap * sizeof(unsigned long long));
+    L.plist_node = off;
+    off = align_up(off + L.plist_cap * sizeof(int));
     L.total = off;
     return L;
 }
@@ -98,6 +103,9 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.gpar = reinterpret_cast<int*>(p + L.gpar);
     w.hb.gstrong = reinterpret_cast<uint8_t*>(p + L.gstrong);
     w.hb.pending = reinterpret_cast<uint8_t*>(p + L.pending);
+    w.hb.plist_idx = reinterpret_cast<unsigned long long*>(p + L.plist_idx);
+    w.hb.plist_node = reinterpret_cast<int*>(p + L.plist_node);
+    w.hb.plist_cap = L.plist_cap;
     return w;
 }
 
@@ -105,6 +113,8 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap) {
     hdr->fix_count = 0;
     hdr->fix_cap = cap;
     hdr->overflow = 0;
+    hdr->plist_count = 0;
+    hdr->plist_overflow = 0;
 }
 
 __global__ void ws_reset_stats_kernel(WsHeader* hdr) {
@@ -216,11 +226,17 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     return EF_OK;
 }
 
-int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws,
-              cudaStream_t st, bool finalize) {
-    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, sm_count_current(), st),
-             "hysteresis");
-    if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, st), "hysteresis finalize");
+// reset: the workspace header has not been initialised by a classify launch of
+// this call (standalone tracing).
+int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
+              cudaStream_t st, bool finalize, bool reset) {
+    const int sms = sm_count_current();
+    if (reset) {
+        ws_begin_kernel<<<1, 1, 0, st>>>(ws.hdr, L.fix_cap);
+        EF_CHECK(cudaGetLastError(), "ws_begin");
+    }
+    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis");
+    if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
     return EF_OK;
 }
 
@@ -285,7 +301,7 @@ int ef_canny_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t wid
     if ((rc = run_classify_u8(d_src, batch, frame_geom(height, width), h_weights, radius, low, high, d_labels,
                               ws, L, st)))
         return rc;
-    return run_trace(d_labels, batch, height, width, d_final, ws, st, true);
+    return run_trace(d_labels, batch, height, width, d_final, ws, L, st, true, false);
 }
 
 int ef_canny_f64(const double* d_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
@@ -302,7 +318,7 @@ int ef_canny_f64(const double* d_src, int64_t batch, int32_t height, int32_t wid
     EF_CHECK(launch_exact<double>(d_src, batch, height, width, XP, d_labels, nullptr, nullptr, nullptr, nullptr,
                                   nullptr, nullptr, nullptr, ws.hdr, st),
              "exact kernel");
-    return run_trace(d_labels, batch, height, width, d_final, ws, st, true);
+    return run_trace(d_labels, batch, height, width, d_final, ws, L, st, true, true);
 }
 
 int ef_trace_edges(const uint8_t* d_labels, int64_t batch, int32_t height, int32_t width, uint8_t* d_final,
@@ -313,7 +329,7 @@ int ef_trace_edges(const uint8_t* d_labels, int64_t batch, int32_t height, int32
     WsLayout L = ws_layout(batch, height, width);
     if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
     Ws ws = ws_bind(d_workspace, L);
-    return run_trace(d_labels, batch, height, width, d_final, ws, (cudaStream_t)stream, true);
+    return run_trace(d_labels, batch, height, width, d_final, ws, L, (cudaStream_t)stream, true, true);
 }
 
 int ef_stages_f64(const uint8_t* d_src8, const double* d_src64, int32_t height, int32_t width,
@@ -485,7 +501,7 @@ int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t f
     FrameGeom g{ht + rows + hb, width, row0 - ht, full_height, row0, rows};
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = run_classify_u8(d_src, 1, g, h_weights, radius, low, high, d_labels, ws, L, st))) return rc;
-    return run_trace(d_labels, 1, rows, width, d_final, ws, st, false);
+    return run_trace(d_labels, 1, rows, width, d_final, ws, L, st, false, false);
 }
 
 int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,
@@ -496,7 +512,7 @@ int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t*
     WsLayout L = ws_layout(1, rows, width);
     if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
     Ws ws = ws_bind(d_workspace, L);
-    return run_trace(d_labels, 1, rows, width, d_final, ws, (cudaStream_t)stream, false);
+    return run_trace(d_labels, 1, rows, width, d_final, ws, L, (cudaStream_t)stream, false, true);
 }
 
 int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows, int32_t width, int64_t* d_ids,
@@ -521,7 +537,8 @@ int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width,
     Ws ws = ws_bind(d_workspace, L);
     cudaStream_t st = (cudaStream_t)stream;
     EF_CHECK(launch_band_apply(rows, width, ws.hb, d_strong_edges, st), "band apply");
-    EF_CHECK(launch_hyst_final(d_labels, 1, rows, width, d_final, ws.hb, st), "hysteresis finalize");
+    EF_CHECK(launch_hyst_final(d_labels, 1, rows, width, d_final, ws.hb, ws.hdr, sm_count_current(), st),
+             "hysteresis finalize");
     return EF_OK;
 }
 

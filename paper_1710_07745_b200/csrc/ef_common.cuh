@@ -44,8 +44,10 @@ struct WsHeader {
     ef_stats stats;          // accumulated counters
     unsigned long long fix_count;
     unsigned long long fix_cap;
-    unsigned int overflow;   // fix list overflowed: fix-up kernel scans all pixels
-    unsigned int pad[7];
+    unsigned long long plist_count;  // hysteresis pending-pixel list (H1 -> H4)
+    unsigned int overflow;           // fix list overflowed: fix-up kernel scans all pixels
+    unsigned int plist_overflow;     // pending list overflowed: H4 re-runs tile CCL
+    unsigned int pad[4];
 };
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

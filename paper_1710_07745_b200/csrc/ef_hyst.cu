@@ -27,7 +27,7 @@ namespace ef {
 
 constexpr int HT = 64;          // tile edge
 constexpr int HP = 4 * HT;      // perimeter slots per tile
-constexpr int H_THREADS = 256;  // 16 pixels per thread
+constexpr int H_THREADS = 128;  // 32 pixels per thread: row = tid/2, columns 32*(tid%2) ..
 constexpr int NO_POS = 0x7fffffff;
 
 struct TileCCL {
@@ -38,7 +38,6 @@ struct TileCCL {
     unsigned char sflag[HT * HT];  // component holds a strong pixel (per root)
     int pending;
     int nodes;
-    int any;
 };
 
 __device__ __forceinline__ int sfind(int* par, int i) {
@@ -137,58 +136,54 @@ __device__ __forceinline__ void pack4(uint32_t w, uint32_t& fg, uint32_t& st) {
     st = (sg * 0x10204080u) >> 28;
 }
 
-// Shared tile CCL used by H1 and H4.  Work is proportional to the foreground:
-// label bytes become per-row bit masks, union-find runs over foreground pixels
-// only.  After return (and a barrier) par[] holds roots for every foreground
-// pixel, sflag[root] marks strong components and minpos[root] the smallest
-// perimeter slot (NO_POS if interior).  Returns this thread's 16-bit
-// foreground mask (row = tid/4, columns 16*(tid%4) ..).
-__device__ uint32_t tile_ccl(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g, TileCCL& s) {
+// Load this thread's 32 label bytes as foreground / strong bit masks and publish
+// the tile's row words.  Also initialises union-find state for its foreground
+// pixels (runs inside the 32-pixel segment pre-linked to their start).
+__device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g,
+                                          TileCCL& s, uint32_t& fg, uint32_t& st) {
     const int tid = threadIdx.x;
-    const int row = tid >> 2, seg = (tid & 3) * 16;
-    const uint8_t* frame = labels + (size_t)g.f * H * W;
-    const int Y = g.y0 + row;
-    uint32_t words[4] = {0u, 0u, 0u, 0u};
-    const uint8_t* src = frame + (size_t)Y * W + g.x0 + seg;
-    if (row < g.vh && seg + 16 <= g.vw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
-        words[0] = q.x; words[1] = q.y; words[2] = q.z; words[3] = q.w;
-    } else if (row < g.vh) {
-        for (int k = 0; k < 16; ++k)
-            if (seg + k < g.vw) words[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
+    const int row = tid >> 1, seg = (tid & 1) * 32;
+    const uint8_t* src = labels + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (row < g.vh && seg + 32 <= g.vw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + 16));
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else if (row < g.vh && seg < g.vw) {
+        const int n = min(32, g.vw - seg);
+        for (int k = 0; k < n; ++k) w[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
     }
-    uint32_t fg = 0, st = 0;
+    fg = 0;
+    st = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
         uint32_t f, t;
-        pack4(words[j], f, t);
+        pack4(w[j], f, t);
         fg |= f << (4 * j);
         st |= t << (4 * j);
     }
-    if (tid == 0) s.any = 0;
-    // segment masks -> row words (4 threads per row, 16 bits each)
-    reinterpret_cast<unsigned short*>(&s.fgrow[row])[tid & 3] = (unsigned short)fg;
-    reinterpret_cast<unsigned short*>(&s.strow[row])[tid & 3] = (unsigned short)st;
-    // init only foreground pixels; runs inside the segment pre-linked to their start
-    {
-        uint32_t m = fg;
-        while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            const int i = row * HT + seg + k;
-            const bool left_in_run = k > 0 && ((fg >> (k - 1)) & 1u);
-            int start = k;
-            if (left_in_run) {  // start of the run containing k inside this segment
-                const uint32_t below = ~fg & ((1u << k) - 1u);
-                start = below ? (32 - __clz(below)) : 0;
-            }
-            s.par[i] = row * HT + seg + start;
-            s.minpos[i] = NO_POS;
-            s.sflag[i] = 0;
-        }
+    reinterpret_cast<uint32_t*>(&s.fgrow[row])[tid & 1] = fg;
+    reinterpret_cast<uint32_t*>(&s.strow[row])[tid & 1] = st;
+    uint32_t m = fg;
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t below = ~fg & ((1u << k) - 1u);
+        const int start = below ? (32 - __clz(below)) : 0;  // start of k's run inside the segment
+        const int i = row * HT + seg + k;
+        s.par[i] = row * HT + seg + start;
+        s.minpos[i] = NO_POS;
+        s.sflag[i] = 0;
     }
-    const int any = __syncthreads_or(fg != 0);
-    if (!any) return 0;
+}
+
+// General tile CCL (foreground holds weak pixels).  After return par[] holds
+// roots for every foreground pixel, sflag[root] marks strong components and
+// minpos[root] the smallest perimeter slot (NO_POS if interior).
+__device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t fg, uint32_t st) {
+    const int tid = threadIdx.x;
+    const int row = tid >> 1, seg = (tid & 1) * 32;
     // unions: W across segments, N / NW / NE from the row above (bit tests)
     const unsigned long long up = row > 0 ? s.fgrow[row - 1] : 0ull;
     const unsigned long long cur = s.fgrow[row];
@@ -210,8 +205,8 @@ __device__ uint32_t tile_ccl(const uint8_t* __restrict__ labels, int H, int W, c
         }
     }
     __syncthreads();
-    // roots into registers first (concurrent path halving may rewrite par[])
-    int roots[16];
+    // roots go to registers first: concurrent path halving may still rewrite par[]
+    int roots[32];
     {
         uint32_t m = fg;
         while (m) {
@@ -235,75 +230,111 @@ __device__ uint32_t tile_ccl(const uint8_t* __restrict__ labels, int H, int W, c
         }
     }
     __syncthreads();
-    return fg;
 }
 
-// 16 bits -> 16 bytes (0/1)
-__device__ __forceinline__ uint4 expand16(uint32_t bits) {
-    uint4 o;
-    o.x = ((bits & 0xFu) * 0x00204081u) & 0x01010101u;
-    o.y = (((bits >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-    o.z = (((bits >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
-    o.w = (((bits >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
-    return o;
-}
-
-__device__ __forceinline__ void store16(uint8_t* dst, int valid, uint4 o) {
-    if (valid >= 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        *reinterpret_cast<uint4*>(dst) = o;
+// 32 bits -> 32 bytes (0/1)
+__device__ __forceinline__ void store32(uint8_t* dst, int valid, uint32_t bits) {
+    uint32_t o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (((bits >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
     } else {
-        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
-        for (int k = 0; k < valid && k < 16; ++k) dst[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+        for (int k = 0; k < valid && k < 32; ++k) dst[k] = (uint8_t)(o[k >> 2] >> (8 * (k & 3)));
     }
 }
 
+// H1: tile-local hysteresis.  Empty tiles write zeros; tiles whose foreground
+// is all strong are final as they stand and export every border pixel as its
+// own strong node (no union-find: anything touching them is strong anyway);
+// other tiles run the shared-memory union-find and append the pixels of
+// undecided border components to the pending list for H4.
 __global__ void __launch_bounds__(H_THREADS)
 hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
-                  uint8_t* __restrict__ final_out, int* __restrict__ perim, int* __restrict__ gpar,
-                  uint8_t* __restrict__ gstrong, uint8_t* __restrict__ pending, WsHeader* hdr) {
+                  uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
     __shared__ TileCCL s;
     const long long tile = tile_id_xyz(tiles_x, tiles_y);
-    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
-    if (threadIdx.x == 0) { s.pending = 0; s.nodes = 0; }
-    const uint32_t fg = tile_ccl(labels, H, W, g, s);
+    const TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
     const int tid = threadIdx.x;
-    const int row = tid >> 2, seg = (tid & 3) * 16;
+    const int row = tid >> 1, seg = (tid & 1) * 32;
+    if (tid == 0) { s.pending = 0; s.nodes = 0; }
+    uint32_t fg, st;
+    tile_load(labels, H, W, g, s, fg, st);
+    const int any_fg = __syncthreads_or(fg != 0);
+    int kind = 0;  // 0 empty, 1 strong-only, 2 general
     uint32_t fin = 0;
-    bool pend = false;
-    {
-        uint32_t m = fg;
-        while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            const int root = s.par[row * HT + seg + k];
-            if (s.sflag[root]) fin |= 1u << k;
-            else if (s.minpos[root] != NO_POS) pend = true;
+    if (any_fg) {
+        kind = __syncthreads_or((fg & ~st) != 0) ? 2 : 1;
+        if (kind == 1) {
+            fin = fg;
+        } else {
+            tile_ccl(g, s, fg, st);
+            uint32_t pend = 0;
+            uint32_t m = fg;
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                const int root = s.par[row * HT + seg + k];
+                if (s.sflag[root]) fin |= 1u << k;
+                else if (s.minpos[root] != NO_POS) pend |= 1u << k;
+            }
+            if (pend) {
+                s.pending = 1;
+                const int cnt = __popc(pend);
+                const unsigned long long at = atomicAdd(&hdr->plist_count, (unsigned long long)cnt);
+                if (at + cnt > b.plist_cap) {
+                    hdr->plist_overflow = 1u;
+                } else {
+                    const unsigned long long base =
+                        (unsigned long long)g.f * H * W + (unsigned long long)(g.y0 + row) * W + g.x0 + seg;
+                    int j = 0;
+                    while (pend) {
+                        const int k = __ffs(pend) - 1;
+                        pend &= pend - 1;
+                        const int root = s.par[row * HT + seg + k];
+                        b.plist_idx[at + j] = base + k;
+                        b.plist_node[at + j] = (int)(tile * HP) + s.minpos[root];
+                        ++j;
+                    }
+                }
+            }
         }
     }
     if (row < g.vh && seg < g.vw)
-        store16(final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg, g.vw - seg, expand16(fin));
-    if (pend) s.pending = 1;
-    // perimeter slot tid: node id of the component at that slot, -1 if background
-    {
-        const int p = tid;  // H_THREADS == HP
+        store32(final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg, g.vw - seg, fin);
+    // perimeter slots p = tid and tid + 128: node id of the component at the slot
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int p = tid + h * H_THREADS;
         int y, x;
         slot_pixel(p, g.vh, g.vw, y, x);
         int node = -1;
         const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
-        if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
-            const int root = s.par[y * HT + x];
-            node = (int)(tile * HP) + s.minpos[root];
-            if (s.minpos[root] == p) {
-                gpar[node] = node;
-                gstrong[node] = s.sflag[root];
-                atomicAdd(&s.nodes, 1);
+        if (kind && valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
+            if (kind == 1) {
+                const int own = perim_slot(y, x, g.vh, g.vw);
+                node = (int)(tile * HP) + own;
+                if (own == p) {
+                    b.gpar[node] = node;
+                    b.gstrong[node] = 1;
+                    atomicAdd(&s.nodes, 1);
+                }
+            } else {
+                const int root = s.par[y * HT + x];
+                node = (int)(tile * HP) + s.minpos[root];
+                if (s.minpos[root] == p) {
+                    b.gpar[node] = node;
+                    b.gstrong[node] = s.sflag[root];
+                    atomicAdd(&s.nodes, 1);
+                }
             }
         }
-        perim[tile * HP + p] = node;
+        b.perim[tile * HP + p] = node;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        pending[tile] = (uint8_t)s.pending;
+    if (tid == 0) {
+        b.pending[tile] = (uint8_t)s.pending;
         if (s.nodes) atomicAdd((unsigned long long*)&hdr->stats.border_nodes, (unsigned long long)s.nodes);
         if (s.pending) atomicAdd((unsigned long long*)&hdr->stats.pending_tiles, 1ull);
     }
@@ -372,27 +403,40 @@ __global__ void hyst_resolve_kernel(long long nslots, const int* __restrict__ pe
     }
 }
 
-// H4: finalise tiles that had undecided border components.
+// H4: pixels of undecided border components read their root's strong flag.
+__global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
+    unsigned long long n = hdr->plist_count;
+    if (n > b.plist_cap) n = b.plist_cap;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (unsigned long long)gridDim.x * blockDim.x)
+        if (b.gstrong[gfind_ro(b.gpar, b.plist_node[e])]) final_out[b.plist_idx[e]] = 1;
+}
+
+// H4 fallback when the pending list overflowed: re-run the tile CCL for every
+// pending tile (same deterministic CCL, so the same nodes).
 __global__ void __launch_bounds__(H_THREADS)
-hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
-                  uint8_t* __restrict__ final_out, const int* __restrict__ gpar,
-                  const uint8_t* __restrict__ gstrong, const uint8_t* __restrict__ pending) {
+hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+                       uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
     __shared__ TileCCL s;
+    if (!hdr->plist_overflow) return;
     const long long tile = tile_id_xyz(tiles_x, tiles_y);
-    if (!pending[tile]) return;
-    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
-    const uint32_t fg = tile_ccl(labels, H, W, g, s);
+    if (!b.pending[tile]) return;
+    const TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
+    uint32_t fg, st;
+    tile_load(labels, H, W, g, s, fg, st);
+    __syncthreads();
+    tile_ccl(g, s, fg, st);
     const int tid = threadIdx.x;
-    const int row = tid >> 2, seg = (tid & 3) * 16;
-    uint32_t m = fg;
+    const int row = tid >> 1, seg = (tid & 1) * 32;
     uint8_t* out = final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
+    uint32_t m = fg;
     while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
         const int root = s.par[row * HT + seg + k];
         if (s.sflag[root] || s.minpos[root] == NO_POS) continue;
         const int node = (int)(tile * HP) + s.minpos[root];
-        if (gstrong[gfind_ro(gpar, node)]) out[k] = 1;
+        if (b.gstrong[gfind_ro(b.gpar, node)]) out[k] = 1;
     }
 }
 
@@ -440,8 +484,7 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                               const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
     const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
-    hyst_local_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
-                                                               b.perim, b.gpar, b.gstrong, b.pending, hdr);
+    hyst_local_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     hyst_merge_kernel<<<tgrid, 128, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b.perim, b.gpar);
@@ -454,11 +497,13 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
 }
 
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, cudaStream_t st) {
+                              const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
+    hyst_final_list_kernel<<<sm_count * 4, 256, 0, st>>>(final_out, b, hdr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     HystLayout L = hyst_layout(batch, H, W);
     const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
-    hyst_final_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
-                                                               b.gpar, b.gstrong, b.pending);
+    hyst_final_tile_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
     return cudaGetLastError();
 }
 

@@ -30,6 +30,9 @@ struct HystBufs {
     int* gpar;
     uint8_t* gstrong;
     uint8_t* pending;
+    unsigned long long* plist_idx;  // pixels of undecided border components (H1 -> H4)
+    int* plist_node;
+    unsigned long long plist_cap;
 };
 
 size_t ex_smem_bytes(int r);
@@ -61,7 +64,7 @@ HystLayout hyst_layout(int64_t batch, int H, int W);
 cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st);
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, cudaStream_t st);
+                              const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st);
 cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
                               cudaStream_t st);
 cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,
