@@ -405,6 +405,9 @@ __global__ void hyst_resolve_kernel(long long nslots, const int* __restrict__ pe
 
 // H4: pixels of undecided border components read their root's strong flag.
 __global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
+    // on overflow the list is incomplete (chunks past the cap were dropped) and
+    // hyst_final_tile_kernel finalises every pending tile instead
+    if (hdr->plist_overflow) return;
     unsigned long long n = hdr->plist_count;
     if (n > b.plist_cap) n = b.plist_cap;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
