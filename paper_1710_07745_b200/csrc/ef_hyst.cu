@@ -28,35 +28,50 @@ namespace ef {
 constexpr int HT = 64;          // tile edge
 constexpr int HP = 4 * HT;      // perimeter slots per tile
 constexpr int H_THREADS = 128;  // 32 pixels per thread: row = tid/2, columns 32*(tid%2) ..
-constexpr int NO_POS = 0x7fffffff;
+constexpr int NO_POS = 0xffff;  // fits the 16-bit minpos entries
 
 struct TileCCL {
     unsigned long long fgrow[HT];  // foreground (label != 0) bit per pixel, one word per row
     unsigned long long strow[HT];  // strong bit per pixel
-    int par[HT * HT];              // union-find parent; initialised for foreground pixels only
-    int minpos[HT * HT];           // smallest perimeter slot per root (foreground only)
+    unsigned short par[HT * HT];     // union-find parent; initialised for foreground pixels only
+    unsigned short minpos[HT * HT];  // smallest perimeter slot per root (foreground only)
     unsigned char sflag[HT * HT];  // component holds a strong pixel (per root)
     int pending;
     int nodes;
 };
 
-__device__ __forceinline__ int sfind(int* par, int i) {
+__device__ __forceinline__ int sfind(unsigned short* par, int i) {
     while (true) {
         int p = par[i];
         if (p == i) return i;
         int gp = par[p];
-        if (gp != p) par[i] = gp;  // path halving: only ever points further up
+        if (gp != p) par[i] = (unsigned short)gp;  // path halving: only ever points further up
         i = p;
     }
 }
 
-__device__ __forceinline__ void sunite(int* par, int a, int b) {
+__device__ __forceinline__ void sunite(unsigned short* par, int a, int b) {
     while (true) {
         a = sfind(par, a);
         b = sfind(par, b);
         if (a == b) return;
         if (a < b) { int t = a; a = b; b = t; }
-        if (atomicCAS(&par[a], a, b) == a) return;
+        if (atomicCAS(&par[a], (unsigned short)a, (unsigned short)b) == (unsigned short)a) return;
+    }
+}
+
+// 16-bit atomic min by CAS on the containing 32-bit word (border pixels only)
+__device__ __forceinline__ void atomic_min_u16(unsigned short* p, unsigned short v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
+    unsigned int old = *w;
+    while (true) {
+        const unsigned short cur = (unsigned short)(old >> sh);
+        if (cur <= v) return;
+        const unsigned int nw = (old & ~(0xffffu << sh)) | ((unsigned int)v << sh);
+        const unsigned int seen = atomicCAS(w, old, nw);
+        if (seen == old) return;
+        old = seen;
     }
 }
 
@@ -172,7 +187,7 @@ __device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, in
         const uint32_t below = ~fg & ((1u << k) - 1u);
         const int start = below ? (32 - __clz(below)) : 0;  // start of k's run inside the segment
         const int i = row * HT + seg + k;
-        s.par[i] = row * HT + seg + start;
+        s.par[i] = (unsigned short)(row * HT + seg + start);
         s.minpos[i] = NO_POS;
         s.sflag[i] = 0;
     }
@@ -217,7 +232,7 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
             roots[k] = r;
             if ((st >> k) & 1u) s.sflag[r] = 1;
             const int p = perim_slot(row, x, g.vh, g.vw);
-            if (p != NO_POS) atomicMin(&s.minpos[r], p);
+            if (p != NO_POS) atomic_min_u16(&s.minpos[r], (unsigned short)p);
         }
     }
     __syncthreads();
@@ -226,7 +241,7 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
         while (m) {
             const int k = __ffs(m) - 1;
             m &= m - 1;
-            s.par[row * HT + seg + k] = roots[k];
+            s.par[row * HT + seg + k] = (unsigned short)roots[k];
         }
     }
     __syncthreads();
@@ -487,6 +502,10 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                               const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
     const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
+    // ~21 KB of shared memory per tile: ask for the full carveout so ~10 tiles
+    // are resident per SM (the kernel is barrier/latency bound)
+    cudaFuncSetAttribute(hyst_local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     hyst_local_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
