@@ -133,6 +133,31 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel_prefix="void k1v2_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
+    kernel, from the committed ncu capture of this bench command
+    (profiles/r01_k1_dram_64frames.csv: `ncu --metrics ...dram__bytes_*...
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`)."""
+    import csv
+
+    path = os.path.join(ROOT, "profiles", "r01_k1_dram_64frames.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+    except OSError:
+        return None
+    hdr, by = None, {}
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d["Kernel Name"].startswith(kernel_prefix) and d["Metric Name"].startswith("dram__bytes_"):
+                by.setdefault(d["ID"], 0.0)
+                by[d["ID"]] += float(d["Metric Value"].replace(",", ""))
+    return round(sum(by.values()) / len(by)) if by else None
+
+
 def cpu_baseline(frames, weights, low, high):
     """Oracle port (oracle/ef_oracle.c: the reference's float64 algorithm in
     C) on the host cores, bounded sample."""
@@ -301,7 +326,10 @@ def run_ours(args):
                        "l2": f"rotating {nbuf} resident input batches ({nbuf * px / 1e6:.0f} MB > 126 MB L2)"},
             "roofline": {"bound": "hbm", "kernel": "k1_classify_kernel (+fix-up launches)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": ncu_traffic() if (args.config == 1 and b == 64 and args.radius == 2) else None,
+                         "traffic_source": "profiles/r01_k1_dram_64frames.csv (ncu dram__bytes_read+write per launch)",
+                         "peak_kind": peak_kind,
                          "alg_bytes_per_launch": int(alg_bytes), "avg_launch_ms": round(k1_ms, 4),
                          "share_of_step": round(k1_ms / ms, 3)},
             "e2e": e2e,

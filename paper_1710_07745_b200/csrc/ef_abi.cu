@@ -410,12 +410,14 @@ int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double*
 // overlap (separate copy engines).
 // ---------------------------------------------------------------------------
 namespace {
+constexpr int kHostStreams = 3;  // H2D, kernels and D2H of three chunks in flight
+
 struct HostCtx {
     std::mutex mu;
     int dev = -1;
-    cudaStream_t st[2] = {nullptr, nullptr};
-    uint8_t* buf[2] = {nullptr, nullptr};  // src | labels | final per stream
-    void* ws[2] = {nullptr, nullptr};
+    cudaStream_t st[kHostStreams] = {};
+    uint8_t* buf[kHostStreams] = {};  // src | labels | final per stream
+    void* ws[kHostStreams] = {};
     size_t buf_px = 0, ws_bytes = 0;
 };
 
@@ -440,21 +442,23 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
     std::lock_guard<std::mutex> lk(C.mu);
     const size_t fpx = (size_t)height * width;
     int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)((8u << 20) / fpx)));
-    if (batch >= 2 && chunk >= batch) chunk = (batch + 1) / 2;
+    if (batch >= kHostStreams && chunk * kHostStreams > batch) chunk = (batch + kHostStreams - 1) / kHostStreams;
+    else if (batch >= 2 && chunk >= batch) chunk = (batch + 1) / 2;
     const size_t need_px = (size_t)chunk * fpx;
     const size_t need_ws = ef_workspace_bytes(chunk, height, width);
     if (C.dev != device) {
         C.dev = device;
-        for (int i = 0; i < 2; ++i) EF_CHECK(cudaStreamCreateWithFlags(&C.st[i], cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < kHostStreams; ++i)
+            EF_CHECK(cudaStreamCreateWithFlags(&C.st[i], cudaStreamNonBlocking), "stream");
     }
     if (C.buf_px < need_px || C.ws_bytes < need_ws) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             if (C.buf[i]) cudaFree(C.buf[i]);
             if (C.ws[i]) cudaFree(C.ws[i]);
             C.buf[i] = nullptr;
             C.ws[i] = nullptr;
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostStreams; ++i) {
             EF_CHECK(cudaMalloc(&C.buf[i], 3 * need_px), "cudaMalloc");
             EF_CHECK(cudaMalloc(&C.ws[i], need_ws), "cudaMalloc");
         }
@@ -462,7 +466,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
         C.ws_bytes = need_ws;
     }
     int k = 0;
-    for (int64_t f0 = 0; f0 < batch; f0 += chunk, k ^= 1) {
+    for (int64_t f0 = 0; f0 < batch; f0 += chunk, k = (k + 1) % kHostStreams) {
         int64_t n = std::min<int64_t>(chunk, batch - f0);
         size_t bytes = (size_t)n * fpx;
         cudaStream_t st = C.st[k];
@@ -476,8 +480,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
         EF_CHECK(cudaMemcpyAsync(h_labels + f0 * fpx, d_lab, bytes, cudaMemcpyDeviceToHost, st), "D2H");
         EF_CHECK(cudaMemcpyAsync(h_final + f0 * fpx, d_fin, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     }
-    EF_CHECK(cudaStreamSynchronize(C.st[0]), "sync");
-    EF_CHECK(cudaStreamSynchronize(C.st[1]), "sync");
+    for (int i = 0; i < kHostStreams; ++i) EF_CHECK(cudaStreamSynchronize(C.st[i]), "sync");
     return EF_OK;
 }
 
