@@ -129,6 +129,8 @@ int check_dims(int64_t batch, int32_t H, int32_t W) {
         return fail(EF_EINVAL, "image dimensions must be >= 1, got batch=" + std::to_string(batch) + " " +
                                    std::to_string(W) + "x" + std::to_string(H));
     if ((unsigned long long)batch * H * W > (1ull << 40)) return fail(EF_EINVAL, "image too large");
+    if (batch > 65535) return fail(EF_EINVAL, "batch > 65535 frames per call (grid z limit); split the batch");
+    if (H > (1 << 22) || W > (1 << 22)) return fail(EF_EINVAL, "frame dimension above 4194304");
     if ((long long)((W + 63) / 64) * ((H + 63) / 64) * batch * 256 >= (1ll << 31))
         return fail(EF_EINVAL, "too many tiles for 32-bit node ids; split the batch");
     return EF_OK;
