@@ -46,7 +46,7 @@ struct V2Smem {
 
 template <int R>
 struct V2Cfg {
-    static constexpr int HXA = R <= 2 ? 4 : 8;
+    static constexpr int HXA = R <= 2 ? 4 : 8;  // R <= 6: one- and two-hop shuffles stay inside the warp
     static constexpr int OW = V2_COLS - 2 * HXA;
     static constexpr int NR = 2 * R + 1;
 };
@@ -161,8 +161,8 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
             v23 = fma2(wf2[o], add2(p[(s + R - o) % NR][1], p[(s + R + o) % NR][1]), v23);
         }
         // horizontal pass: neighbours' pairs by 64-bit shuffles
-        // e[j] = column c - 4 + j, j = 0..11 (lane-1's 4, own 4, lane+1's 4)
-        float e[12];
+        // e[j] = column c - 8 + j, j = 0..19 (lanes -2..+2; lane +-2 only for R > 4)
+        float e[20];
         {
             const double d01 = __hiloint2double(__float_as_int(v01.y), __float_as_int(v01.x));
             const double d23 = __hiloint2double(__float_as_int(v23.y), __float_as_int(v23.x));
@@ -170,25 +170,30 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
             const double r01 = __shfl_down_sync(0xffffffffu, d01, 1);
             const double l01 = R > 2 ? __shfl_up_sync(0xffffffffu, d01, 1) : 0.0;
             const double r23 = R > 2 ? __shfl_down_sync(0xffffffffu, d23, 1) : 0.0;
-            e[0] = __int_as_float(__double2loint(l01)); e[1] = __int_as_float(__double2hiint(l01));
-            e[2] = __int_as_float(__double2loint(l23)); e[3] = __int_as_float(__double2hiint(l23));
-            e[4] = v01.x; e[5] = v01.y; e[6] = v23.x; e[7] = v23.y;
-            e[8] = __int_as_float(__double2loint(r01)); e[9] = __int_as_float(__double2hiint(r01));
-            e[10] = __int_as_float(__double2loint(r23)); e[11] = __int_as_float(__double2hiint(r23));
+            const double ll23 = R > 4 ? __shfl_up_sync(0xffffffffu, d23, 2) : 0.0;
+            const double rr01 = R > 4 ? __shfl_down_sync(0xffffffffu, d01, 2) : 0.0;
+            e[2] = __int_as_float(__double2loint(ll23)); e[3] = __int_as_float(__double2hiint(ll23));
+            e[4] = __int_as_float(__double2loint(l01)); e[5] = __int_as_float(__double2hiint(l01));
+            e[6] = __int_as_float(__double2loint(l23)); e[7] = __int_as_float(__double2hiint(l23));
+            e[8] = v01.x; e[9] = v01.y; e[10] = v23.x; e[11] = v23.y;
+            e[12] = __int_as_float(__double2loint(r01)); e[13] = __int_as_float(__double2hiint(r01));
+            e[14] = __int_as_float(__double2loint(r23)); e[15] = __int_as_float(__double2hiint(r23));
+            e[16] = __int_as_float(__double2loint(rr01)); e[17] = __int_as_float(__double2hiint(rr01));
+            e[0] = e[1] = e[18] = e[19] = 0.f;
         }
-        // b(k) = w0 e[4+k] + sum_o w_o (e[4+k-o] + e[4+k+o]); even o on aligned pairs
-        float2 b01 = mul2(wf2[0], f2(e[4], e[5]));
-        float2 b23 = mul2(wf2[0], f2(e[6], e[7]));
+        // b(k) = w0 e[8+k] + sum_o w_o (e[8+k-o] + e[8+k+o]); even o on aligned pairs
+        float2 b01 = mul2(wf2[0], f2(e[8], e[9]));
+        float2 b23 = mul2(wf2[0], f2(e[10], e[11]));
 #pragma unroll
         for (int o = 1; o <= R; ++o) {
             if ((o & 1) == 0) {
-                b01 = fma2(wf2[o], add2(f2(e[4 - o], e[5 - o]), f2(e[4 + o], e[5 + o])), b01);
-                b23 = fma2(wf2[o], add2(f2(e[6 - o], e[7 - o]), f2(e[6 + o], e[7 + o])), b23);
+                b01 = fma2(wf2[o], add2(f2(e[8 - o], e[9 - o]), f2(e[8 + o], e[9 + o])), b01);
+                b23 = fma2(wf2[o], add2(f2(e[10 - o], e[11 - o]), f2(e[10 + o], e[11 + o])), b23);
             } else {
-                b01.x = fmaf(wf2[o].x, e[4 - o] + e[4 + o], b01.x);
-                b01.y = fmaf(wf2[o].x, e[5 - o] + e[5 + o], b01.y);
-                b23.x = fmaf(wf2[o].x, e[6 - o] + e[6 + o], b23.x);
-                b23.y = fmaf(wf2[o].x, e[7 - o] + e[7 + o], b23.y);
+                b01.x = fmaf(wf2[o].x, e[8 - o] + e[8 + o], b01.x);
+                b01.y = fmaf(wf2[o].x, e[9 - o] + e[9 + o], b01.y);
+                b23.x = fmaf(wf2[o].x, e[10 - o] + e[10 + o], b23.x);
+                b23.y = fmaf(wf2[o].x, e[11 - o] + e[11 + o], b23.y);
             }
         }
         float b[4] = {b01.x, b01.y, b23.x, b23.y};
@@ -444,7 +449,7 @@ k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     }
 }
 
-bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 4 && (g.W % 4) == 0; }
+bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 6 && (g.W % 4) == 0; }
 
 template <int R>
 static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
@@ -468,6 +473,8 @@ cudaError_t launch_k1v2(const uint8_t* src, int64_t batch, const FrameGeom& g, c
         case 2: return launch_r<2>(src, batch, g, P, labels, fix_list, hdr, st);
         case 3: return launch_r<3>(src, batch, g, P, labels, fix_list, hdr, st);
         case 4: return launch_r<4>(src, batch, g, P, labels, fix_list, hdr, st);
+        case 5: return launch_r<5>(src, batch, g, P, labels, fix_list, hdr, st);
+        case 6: return launch_r<6>(src, batch, g, P, labels, fix_list, hdr, st);
         default: return cudaErrorInvalidValue;
     }
 }
