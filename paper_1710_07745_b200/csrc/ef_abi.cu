@@ -56,8 +56,8 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
-    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, total;
-    unsigned long long fix_cap, plist_cap;
+    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, node_list, total;
+    unsigned long long fix_cap, plist_cap, node_cap;
     HystLayout hl;
 };
 
@@ -84,6 +84,9 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     off = align_up(off + L.plist_cap * sizeof(unsigned long long));
     L.plist_node = off;
     off = align_up(off + L.plist_cap * sizeof(int));
+    L.node_cap = std::max<unsigned long long>(1ull << 16, (unsigned long long)L.hl.slots / 8);
+    L.node_list = off;
+    off = align_up(off + L.node_cap * sizeof(int));
     L.total = off;
     return L;
 }
@@ -106,6 +109,8 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.plist_idx = reinterpret_cast<unsigned long long*>(p + L.plist_idx);
     w.hb.plist_node = reinterpret_cast<int*>(p + L.plist_node);
     w.hb.plist_cap = L.plist_cap;
+    w.hb.node_list = reinterpret_cast<int*>(p + L.node_list);
+    w.hb.node_cap = L.node_cap;
     return w;
 }
 
@@ -115,6 +120,8 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap) {
     hdr->overflow = 0;
     hdr->plist_count = 0;
     hdr->plist_overflow = 0;
+    hdr->node_count = 0;
+    hdr->node_overflow = 0;
 }
 
 __global__ void ws_reset_stats_kernel(WsHeader* hdr) {

@@ -348,6 +348,24 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
         b.perim[tile * HP + p] = node;
     }
     __syncthreads();
+    // this tile's nodes are the slots with perim[slot] == own id; list them for H3
+    if (s.nodes) {
+        __shared__ unsigned long long nbase;
+        if (tid == 0) nbase = atomicAdd(&hdr->node_count, (unsigned long long)s.nodes);
+        __syncthreads();
+        if (nbase + s.nodes <= b.node_cap) {
+            __shared__ int ncur;
+            if (tid == 0) ncur = 0;
+            __syncthreads();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int p = tid + h * H_THREADS;
+                if (b.perim[tile * HP + p] == (int)(tile * HP) + p) b.node_list[nbase + atomicAdd(&ncur, 1)] = (int)(tile * HP) + p;
+            }
+        } else if (tid == 0) {
+            hdr->node_overflow = 1u;
+        }
+    }
     if (tid == 0) {
         b.pending[tile] = (uint8_t)s.pending;
         if (s.nodes) atomicAdd((unsigned long long*)&hdr->stats.border_nodes, (unsigned long long)s.nodes);
@@ -406,15 +424,21 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, const int* __restrict_
     }
 }
 
-// H3: strong flag of every node onto its root.
-__global__ void hyst_resolve_kernel(long long nslots, const int* __restrict__ perim, int* gpar,
-                                    uint8_t* gstrong) {
-    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
-         s += (long long)gridDim.x * blockDim.x) {
-        int n = perim[s];
-        if (n != (int)s) continue;  // the node's own (smallest) slot only
-        int r = gfind(gpar, n);
-        if (gstrong[n] && r != n) gstrong[r] = 1;
+// H3: strong flag of every node onto its root (over H1's node list; every
+// perimeter slot if that list overflowed).
+__global__ void hyst_resolve_kernel(long long nslots, HystBufs b, const WsHeader* __restrict__ hdr) {
+    const bool all = hdr->node_overflow != 0;
+    const long long n = all ? nslots : (long long)hdr->node_count;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        int node;
+        if (all) {
+            node = b.perim[e];
+            if (node != (int)e) continue;  // the node's own (smallest) slot only
+        } else {
+            node = b.node_list[e];
+        }
+        const int r = gfind(b.gpar, node);
+        if (b.gstrong[node] && r != node) b.gstrong[r] = 1;
     }
 }
 
@@ -430,16 +454,28 @@ __global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs
         if (b.gstrong[gfind_ro(b.gpar, b.plist_node[e])]) final_out[b.plist_idx[e]] = 1;
 }
 
+struct TileCCL;
+__device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+                                uint8_t* __restrict__ final_out, const HystBufs& b, long long tile, TileCCL& s);
+
 // H4 fallback when the pending list overflowed: re-run the tile CCL for every
 // pending tile (same deterministic CCL, so the same nodes).
 __global__ void __launch_bounds__(H_THREADS)
-hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, int frames,
                        uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
     __shared__ TileCCL s;
     if (!hdr->plist_overflow) return;
-    const long long tile = tile_id_xyz(tiles_x, tiles_y);
-    if (!b.pending[tile]) return;
-    const TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
+    const long long ntiles = (long long)tiles_x * tiles_y * frames;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (b.pending[tile]) hyst_final_tile(labels, H, W, tiles_x, tiles_y, final_out, b, tile, s);
+    }
+}
+
+__device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+                                uint8_t* __restrict__ final_out, const HystBufs& b, long long tile, TileCCL& s) {
+    const int txi = (int)(tile % tiles_x);
+    const long long rest = tile / tiles_x;
+    const TileGeo g = tile_geo_xyz(txi, (int)(rest % tiles_y), (int)(rest / tiles_y), H, W);
     uint32_t fg, st;
     tile_load(labels, H, W, g, s, fg, st);
     __syncthreads();
@@ -456,6 +492,7 @@ hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         const int node = (int)(tile * HP) + s.minpos[root];
         if (b.gstrong[gfind_ro(b.gpar, node)]) out[k] = 1;
     }
+    __syncthreads();  // shared state is reused by the next tile of this block
 }
 
 // Band edge export: component root id and strong flag for the top and bottom
@@ -514,7 +551,7 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
     if (e != cudaSuccess) return e;
     long long blocks = (L.slots + 255) / 256;
     if (blocks > (long long)sm_count * 16) blocks = (long long)sm_count * 16;
-    hyst_resolve_kernel<<<(unsigned)blocks, 256, 0, st>>>(L.slots, b.perim, b.gpar, b.gstrong);
+    hyst_resolve_kernel<<<(unsigned)blocks, 256, 0, st>>>(L.slots, b, hdr);
     return cudaGetLastError();
 }
 
@@ -524,8 +561,8 @@ cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     HystLayout L = hyst_layout(batch, H, W);
-    const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
-    hyst_final_tile_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
+    hyst_final_tile_kernel<<<sm_count * 2, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, (int)batch,
+                                                               final_out, b, hdr);
     return cudaGetLastError();
 }
 

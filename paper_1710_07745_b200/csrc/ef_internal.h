@@ -33,6 +33,8 @@ struct HystBufs {
     unsigned long long* plist_idx;  // pixels of undecided border components (H1 -> H4)
     int* plist_node;
     unsigned long long plist_cap;
+    int* node_list;  // border-component node ids (H1 -> H3)
+    unsigned long long node_cap;
 };
 
 size_t ex_smem_bytes(int r);
