@@ -24,6 +24,12 @@
 // load; blurred and magnitude values at out-of-frame columns are replaced by
 // the edge column's value (warp shuffle); magnitude rows -1 and H alias rows
 // 0 and H-1 in the ring.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
 #include "ef_common.cuh"
 #include "ef_internal.h"
 
@@ -38,10 +44,21 @@ constexpr int V2_ROWS_PER_WARP = V2_TH / V2_WARPS;
 constexpr int MRING = 8;
 constexpr int QCAP = 128;
 
+constexpr int V2_MAXR = 6;
+constexpr int V2_IN_ROWS = V2_BROWS + 2 * V2_MAXR;  // staged u8 input rows (TMA box height <= this)
+// TMA box starts must be 16-byte aligned in the innermost (column) dimension
+// (an unaligned start faults with "illegal instruction" on sm_100a), so the
+// staged box starts at xv0 & ~15 and is 16 columns wider than the tile.
+constexpr int V2_IN_COLS = V2_COLS + 16;
+
 struct V2Smem {
     float b[V2_BROWS][V2_COLS];
-    float m[V2_WARPS][MRING][V2_COLS];
+    union {
+        float m[V2_WARPS][MRING][V2_COLS];            // phase 2: magnitude rings
+        unsigned char in[V2_IN_ROWS][V2_IN_COLS];     // phase 1: TMA-staged input tile + halo
+    };
     int q[V2_WARPS][QCAP];
+    unsigned long long mbar;                           // TMA completion barrier
 };
 
 template <int R>
@@ -108,7 +125,7 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 // Rows of b computed per warp in phase 1: the tile's 68 b rows split 4 ways.
 constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 17
 
-template <int R, bool INTERIOR>
+template <int R, bool INTERIOR, bool STAGED>
 __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const FrameGeom& g, int xv0, int y0,
                                           const FastParams& P, V2Smem& S, int warp, int lane) {
     constexpr int NR = V2Cfg<R>::NR;
@@ -127,6 +144,11 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
     const uint8_t* base = img - (ptrdiff_t)g.g0 * W;
     // interior tiles never clamp (all input rows exist); 32-bit row offsets
     auto rowp = [&](int Y) { return base + (INTERIOR ? Y : min(max(Y, rlo), rhi)) * W; };
+    // STAGED: the whole input tile (rows y0-2-R ..) is in shared memory already
+    auto in_row = [&](int Y) -> uint32_t {
+        return *reinterpret_cast<const uint32_t*>(&S.in[Y - (y0 - 2 - R)][(xv0 & 15) + 4 * lane]);
+    };
+    auto fetch = [&](int Y) -> uint32_t { return STAGED ? in_row(Y) : load4(rowp(Y), c, W, col_ok); };
     float2 wf2[R + 1];
 #pragma unroll
     for (int k = 0; k <= R; ++k) wf2[k] = f2(P.wf[k], P.wf[k]);
@@ -142,16 +164,16 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
     uint32_t raw[NR];
     // input row ii is global row ys - R + ii
 #pragma unroll
-    for (int ii = 0; ii < 2 * R; ++ii) cvt(load4(rowp(ys - R + ii), c, W, col_ok), p[ii][0], p[ii][1]);
+    for (int ii = 0; ii < 2 * R; ++ii) cvt(fetch(ys - R + ii), p[ii][0], p[ii][1]);
 #pragma unroll
-    for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = load4(rowp(ys - R + ii), c, W, col_ok);
+    for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = fetch(ys - R + ii);
     float* out = &S.b[ys - (y0 - 2)][4 * lane];
 
 #pragma unroll
     for (int u = 0; u < V2_P1_ROWS; ++u) {
         const int s = u % NR;
         cvt(raw[(s + 2 * R) % NR], p[(s + 2 * R) % NR][0], p[(s + 2 * R) % NR][1]);
-        if (u + 2 * R < V2_P1_ROWS) raw[(s + 4 * R) % NR] = load4(rowp(ys - R + u + 4 * R), c, W, col_ok);
+        if (u + 2 * R < V2_P1_ROWS) raw[(s + 4 * R) % NR] = fetch(ys - R + u + 4 * R);
         // vertical pass on column pairs
         float2 v01 = mul2(wf2[0], p[(s + R) % NR][0]);
         float2 v23 = mul2(wf2[0], p[(s + R) % NR][1]);
@@ -422,10 +444,15 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
     }
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 template <int R>
 __global__ void __launch_bounds__(V2_THREADS, 6)
 k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
-            unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr) {
+            unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
+            const __grid_constant__ CUtensorMap tmap, int use_tma) {
     extern __shared__ __align__(16) unsigned char smraw[];
     V2Smem& S = *reinterpret_cast<V2Smem*>(smraw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -438,18 +465,78 @@ k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     // every output row is classified -- no clamps, no predicated stores
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
-    if (interior) {
-        v2_phase1<R, true>(img, g, xv0, y0, P, S, warp, lane);
+    if (interior && use_tma) {
+        // TMA: the u8 tile + halo (128 columns x TH+4+2R rows of frame z) lands in
+        // shared memory in one bulk tensor copy; completion on an mbarrier.
+        constexpr int rows = V2_BROWS + 2 * R;
+        const uint32_t bar = smem_u32(&S.mbar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // init visible to the TMA unit
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * V2_IN_COLS)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+                    "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
+                    "r"(bar)
+                : "memory");
+        }
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(bar)
+                : "memory");
+        }
+        v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
+        __syncthreads();
+        v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
+    } else if (interior) {
+        v2_phase1<R, true, false>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
         v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
     } else {
-        v2_phase1<R, false>(img, g, xv0, y0, P, S, warp, lane);
+        v2_phase1<R, false, false>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
         v2_phase2<R, false>(g, xv0, y0, P, S, warp, lane, O);
     }
 }
 
 bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 6 && (g.W % 4) == 0; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D map (column, buffer row, frame) over the u8 source; box = 144 columns x
+// (TH + 4 + 2R) rows.  TMA needs 16-byte aligned rows: W % 16 == 0.
+static bool make_src_map(CUtensorMap& tm, const uint8_t* src, int64_t batch, const FrameGeom& g, int R) {
+    auto enc = tensor_map_encoder();
+    if (!enc || (g.W % 16) != 0 || (reinterpret_cast<uintptr_t>(src) & 15) != 0) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)g.W, (cuuint64_t)g.W * g.H};
+    cuuint32_t box[3] = {(cuuint32_t)V2_IN_COLS, (cuuint32_t)(V2_BROWS + 2 * R), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 template <int R>
 static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
@@ -462,7 +549,10 @@ static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& 
                              (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     dim3 grid((g.W + V2Cfg<R>::OW - 1) / V2Cfg<R>::OW, (g.rows + V2_TH - 1) / V2_TH, (unsigned)batch);
-    k1v2_kernel<R><<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr);
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof tm);
+    const int use_tma = make_src_map(tm, src, batch, g, R) && !getenv("EF_NO_TMA");
+    k1v2_kernel<R><<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr, tm, use_tma);
     return cudaGetLastError();
 }
 
