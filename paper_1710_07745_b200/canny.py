@@ -241,6 +241,9 @@ def canny_u8_host(frames: np.ndarray, weights, low: float, high: float, labels: 
     b, h, w = x.shape
     labels = np.empty(x.shape, np.uint8) if labels is None else labels
     final = np.empty(x.shape, np.uint8) if final is None else final
+    for name, a in (("labels", labels), ("final", final)):
+        if (a.shape != x.shape or a.dtype != np.uint8 or not a.flags.c_contiguous or not a.flags.writeable):
+            raise ValueError(f"{name} must be a writeable C-contiguous uint8 array of shape {x.shape}")
     _, wp, r = host_weights(weights)
     dev = torch.cuda.current_device() if device is None else int(device)
     rc = _lib.load().ef_canny_u8_host(x.ctypes.data, b, h, w, wp, r, float(low), float(high),

@@ -15,6 +15,7 @@
 
 #include "ef_common.cuh"
 #include "ef_internal.h"
+#include "ef_host.h"
 
 using namespace ef;
 
@@ -414,20 +415,52 @@ int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double*
 }
 
 // ---------------------------------------------------------------------------
-// Host-buffer pipeline: chunks of frames round-robin over two streams so the
-// H2D copy of chunk i+1, the kernels of chunk i and the D2H of chunk i-1
-// overlap (separate copy engines).
+// Host-buffer pipeline (the drop-in's path: run_pipeline returns host arrays).
+// Chunks of frames round-robin over three streams so the H2D copy of chunk
+// i+1, the kernels of chunk i and the D2H of chunk i-1 overlap.  The output
+// crosses PCIe packed to 2 bits per pixel and is expanded into the caller's
+// labels/final arrays by a host thread pool (ef_host.cu); pageable inputs are
+// staged into pinned memory by the same pool.
+//
+// Measured on the B200 box (16-core VM, tools/host_bw.cu, tools/e2e_probe.py):
+//  * host DRAM bandwidth is what binds -- the DMA reading the input and the
+//    unpack writing 2 B/px share it, so the unpack of a chunk that overlaps
+//    copies uses 4 threads (more only slows the DMA), the last chunk all;
+//  * the packed staging lines are flushed from the CPU caches after the unpack:
+//    DMA writes into CPU-cached pinned lines ran ~3x slower and dragged the
+//    concurrent H2D down with them;
+//  * chunks ramp 2 -> 16 MB and back down, so the pipeline fills and drains
+//    quickly while the middle chunks are large enough for the kernels to keep
+//    up with the copy engine.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int kHostStreams = 3;  // H2D, kernels and D2H of three chunks in flight
+constexpr int kHostStreams = 3;
+constexpr int kPackSlots = 2 * kHostStreams;  // packed chunks in flight (D2H or unpack)
+constexpr int kOverlapUnpackThreads = 4;
+
+struct PackSlot {
+    uint8_t* packed = nullptr;   // pinned
+    cudaEvent_t done = nullptr;  // recorded after the packed D2H
+    Latch latch;
+    bool failed = false;
+    bool last = false;  // last chunk of the call: unpack with every pool thread
+    size_t nbytes = 0, npx = 0;
+    uint8_t* labels = nullptr;
+    uint8_t* final_map = nullptr;
+    bool used = false;
+};
 
 struct HostCtx {
     std::mutex mu;
     int dev = -1;
     cudaStream_t st[kHostStreams] = {};
-    uint8_t* buf[kHostStreams] = {};  // src | labels | final per stream
+    uint8_t* buf[kHostStreams] = {};  // src | labels | final | packed per stream
     void* ws[kHostStreams] = {};
-    size_t buf_px = 0, ws_bytes = 0;
+    uint8_t* stage[kHostStreams] = {};  // pinned staging for pageable inputs
+    cudaEvent_t h2d[kHostStreams] = {};
+    bool h2d_pending[kHostStreams] = {};
+    size_t buf_px = 0, ws_bytes = 0, stage_bytes = 0, slot_bytes = 0;
+    PackSlot slot[kPackSlots];
 };
 
 HostCtx& host_ctx(int dev) {
@@ -437,6 +470,95 @@ HostCtx& host_ctx(int dev) {
     auto& p = ctxs[dev];
     if (!p) p = new HostCtx();
     return *p;
+}
+
+void unpack_part(PackSlot* s, size_t b0, size_t b1) {
+    unpack_codes(s->packed, b0, b1, s->npx, s->labels, s->final_map);
+    flush_lines(s->packed + b0, b1 - b0);
+}
+
+// Pool task: wait for the chunk's packed D2H, then fan the unpack out over the
+// pool.  (An event wait, not cudaLaunchHostFunc: a host callback would stall
+// the stream -- and the next chunk's H2D behind it -- until it returns.)
+void wait_and_unpack(PackSlot* s, int device) {
+    cudaSetDevice(device);
+    if (cudaEventSynchronize(s->done) != cudaSuccess) {
+        s->failed = true;
+        s->latch.done();
+        return;
+    }
+    HostPool& P = host_pool();
+    const size_t threads = s->last ? (size_t)P.size() : (size_t)std::min(P.size(), kOverlapUnpackThreads);
+    const size_t parts = std::max<size_t>(1, std::min<size_t>(threads, s->nbytes / 16384));
+    const size_t per = ((s->nbytes + parts - 1) / parts + 63) & ~size_t(63);
+    const int n = (int)((s->nbytes + per - 1) / per);
+    s->latch.add(n - 1);
+    for (size_t b0 = per; b0 < s->nbytes; b0 += per) {
+        const size_t b1 = std::min(s->nbytes, b0 + per);
+        P.submit([s, b0, b1] {
+            unpack_part(s, b0, b1);
+            s->latch.done();
+        }, true);
+    }
+    unpack_part(s, 0, std::min(s->nbytes, per));
+    s->latch.done();
+}
+
+// 0: pinned host (DMA directly), 1: pageable (stage), 2: device/managed
+int host_kind(const void* p, size_t bytes) {
+    cudaPointerAttributes a;
+    auto kind = [&](const void* q) {
+        if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+            cudaGetLastError();
+            return 1;
+        }
+        if (a.type == cudaMemoryTypeHost) return 0;
+        if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return 2;
+        return 1;
+    };
+    const int k0 = kind(p);
+    if (k0 == 1 || bytes <= 1) return k0;
+    return kind(static_cast<const uint8_t*>(p) + bytes - 1) == k0 ? k0 : 1;
+}
+
+// wait until every queued chunk has landed in the caller's arrays
+bool drain(HostCtx& C) {
+    for (int i = 0; i < kHostStreams; ++i)
+        if (C.st[i]) cudaStreamSynchronize(C.st[i]);
+    bool failed = false;
+    for (auto& s : C.slot) {
+        if (!s.used) continue;
+        s.latch.wait();
+        failed |= s.failed;
+        s.used = false;
+    }
+    for (int i = 0; i < kHostStreams; ++i) C.h2d_pending[i] = false;
+    return failed;
+}
+
+// frames per chunk: ramp up from ~2 MB to ~16 MB, hold, ramp back down
+std::vector<int64_t> chunk_plan(int64_t batch, size_t fpx) {
+    const int64_t cmax = std::max<int64_t>(1, (int64_t)((16u << 20) / fpx));
+    const int64_t c0 = std::max<int64_t>(1, std::min<int64_t>(cmax, (int64_t)((2u << 20) / fpx)));
+    std::vector<int64_t> ramp;
+    for (int64_t c = c0; c < cmax; c *= 2) ramp.push_back(c);
+    int64_t ramp_sum = 0;
+    for (int64_t c : ramp) ramp_sum += c;
+    std::vector<int64_t> plan;
+    if (2 * ramp_sum + cmax > batch) {  // short batch: up to three near-equal chunks of <= cmax
+        const int64_t n = std::max<int64_t>(std::min<int64_t>(batch, kHostStreams), (batch + cmax - 1) / cmax);
+        for (int64_t i = 0; i < n; ++i) plan.push_back(batch / n + (i < batch % n ? 1 : 0));
+        return plan;
+    }
+    plan = ramp;
+    int64_t mid = batch - 2 * ramp_sum;
+    while (mid > 0) {
+        const int64_t c = std::min(mid, cmax);
+        plan.push_back(c);
+        mid -= c;
+    }
+    plan.insert(plan.end(), ramp.rbegin(), ramp.rend());
+    return plan;
 }
 }  // namespace
 
@@ -450,15 +572,22 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
     HostCtx& C = host_ctx(device);
     std::lock_guard<std::mutex> lk(C.mu);
     const size_t fpx = (size_t)height * width;
-    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)((8u << 20) / fpx)));
-    if (batch >= kHostStreams && chunk * kHostStreams > batch) chunk = (batch + kHostStreams - 1) / kHostStreams;
-    else if (batch >= 2 && chunk >= batch) chunk = (batch + 1) / 2;
-    const size_t need_px = (size_t)chunk * fpx;
+    const std::vector<int64_t> plan = chunk_plan(batch, fpx);
+    const int64_t chunk = *std::max_element(plan.begin(), plan.end());
+    const size_t need_px = align_up((size_t)chunk * fpx);
+    const size_t need_packed = align_up(need_px / 4 + 1);
     const size_t need_ws = ef_workspace_bytes(chunk, height, width);
+    const int src_kind = host_kind(h_src, (size_t)batch * fpx);
     if (C.dev != device) {
         C.dev = device;
-        for (int i = 0; i < kHostStreams; ++i)
+        // blocking-sync events: a pool thread waiting on a chunk sleeps instead
+        // of spinning on a core the unpack needs
+        for (int i = 0; i < kHostStreams; ++i) {
             EF_CHECK(cudaStreamCreateWithFlags(&C.st[i], cudaStreamNonBlocking), "stream");
+            EF_CHECK(cudaEventCreateWithFlags(&C.h2d[i], cudaEventDisableTiming | cudaEventBlockingSync), "event");
+        }
+        for (auto& s : C.slot)
+            EF_CHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming | cudaEventBlockingSync), "event");
     }
     if (C.buf_px < need_px || C.ws_bytes < need_ws) {
         for (int i = 0; i < kHostStreams; ++i) {
@@ -467,29 +596,100 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
             C.buf[i] = nullptr;
             C.ws[i] = nullptr;
         }
+        C.buf_px = C.ws_bytes = 0;
         for (int i = 0; i < kHostStreams; ++i) {
-            EF_CHECK(cudaMalloc(&C.buf[i], 3 * need_px), "cudaMalloc");
+            EF_CHECK(cudaMalloc(&C.buf[i], 3 * need_px + need_packed), "cudaMalloc");
             EF_CHECK(cudaMalloc(&C.ws[i], need_ws), "cudaMalloc");
         }
         C.buf_px = need_px;
         C.ws_bytes = need_ws;
     }
-    int k = 0;
-    for (int64_t f0 = 0; f0 < batch; f0 += chunk, k = (k + 1) % kHostStreams) {
-        int64_t n = std::min<int64_t>(chunk, batch - f0);
-        size_t bytes = (size_t)n * fpx;
+    if (C.slot_bytes < need_packed) {
+        for (auto& s : C.slot) {
+            if (s.packed) cudaFreeHost(s.packed);
+            s.packed = nullptr;
+        }
+        C.slot_bytes = 0;
+        for (auto& s : C.slot) EF_CHECK(cudaMallocHost(&s.packed, need_packed), "cudaMallocHost");
+        C.slot_bytes = need_packed;
+    }
+    if (src_kind == 1 && C.stage_bytes < need_px) {
+        for (int i = 0; i < kHostStreams; ++i) {
+            if (C.stage[i]) cudaFreeHost(C.stage[i]);
+            C.stage[i] = nullptr;
+        }
+        C.stage_bytes = 0;
+        for (int i = 0; i < kHostStreams; ++i) EF_CHECK(cudaMallocHost(&C.stage[i], need_px), "cudaMallocHost");
+        C.stage_bytes = need_px;
+    }
+    const int sms = sm_count_current();
+    int64_t f0 = 0;
+    for (size_t i = 0; i < plan.size(); f0 += plan[i], ++i) {
+        const int k = (int)(i % kHostStreams);
+        PackSlot& s = C.slot[i % kPackSlots];
+        const int64_t n = plan[i];
+        const size_t bytes = (size_t)n * fpx;
         cudaStream_t st = C.st[k];
         uint8_t* d_src = C.buf[k];
         uint8_t* d_lab = d_src + C.buf_px;
         uint8_t* d_fin = d_lab + C.buf_px;
-        EF_CHECK(cudaMemcpyAsync(d_src, h_src + f0 * fpx, bytes, cudaMemcpyHostToDevice, st), "H2D");
+        uint8_t* d_packed = d_fin + C.buf_px;
+        cudaError_t e = cudaSuccess;
+        if (s.used) {  // the slot's previous chunk must be unpacked before its D2H is overwritten
+            s.latch.wait();
+            s.used = false;
+            if (s.failed) e = cudaErrorUnknown;
+        }
+        const uint8_t* src = h_src + f0 * fpx;
+        if (e == cudaSuccess && src_kind == 1) {
+            if (C.h2d_pending[k]) e = cudaEventSynchronize(C.h2d[k]);
+            if (e == cudaSuccess) parallel_copy(C.stage[k], src, bytes);
+            src = C.stage[k];
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_src, src, bytes, src_kind == 2 ? cudaMemcpyDefault : cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && src_kind == 1) {
+            e = cudaEventRecord(C.h2d[k], st);
+            C.h2d_pending[k] = true;
+        }
+        if (e != cudaSuccess) {
+            drain(C);
+            return cuda_fail(e, "H2D");
+        }
         if ((rc = ef_canny_u8(d_src, n, height, width, h_weights, radius, low, high, d_lab, d_fin, C.ws[k],
-                              C.ws_bytes, st)))
+                              C.ws_bytes, st))) {
+            drain(C);
             return rc;
-        EF_CHECK(cudaMemcpyAsync(h_labels + f0 * fpx, d_lab, bytes, cudaMemcpyDeviceToHost, st), "D2H");
-        EF_CHECK(cudaMemcpyAsync(h_final + f0 * fpx, d_fin, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        const size_t pbytes = (bytes + 3) / 4;
+        e = launch_pack(d_lab, d_fin, (long long)bytes, d_packed, sms, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(s.packed, d_packed, pbytes, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) {
+            s.nbytes = pbytes;
+            s.npx = bytes;
+            s.labels = h_labels + f0 * fpx;
+            s.final_map = h_final + f0 * fpx;
+            s.last = i + 1 == plan.size();
+            e = cudaEventRecord(s.done, st);
+        }
+        if (e != cudaSuccess) {
+            drain(C);
+            return cuda_fail(e, "D2H");
+        }
+        s.used = true;
+        s.failed = false;
+        s.latch.add(1);
+        PackSlot* sp = &s;
+        host_pool().submit([sp, device] { wait_and_unpack(sp, device); });
     }
-    for (int i = 0; i < kHostStreams; ++i) EF_CHECK(cudaStreamSynchronize(C.st[i]), "sync");
+    cudaError_t first = cudaSuccess;
+    for (int k = 0; k < kHostStreams; ++k) {
+        cudaError_t e = cudaStreamSynchronize(C.st[k]);
+        if (first == cudaSuccess) first = e;
+    }
+    const bool failed = drain(C);
+    if (first != cudaSuccess) return cuda_fail(first, "sync");
+    if (failed) return fail(EF_ECUDA, "D2H of packed edges failed");
     return EF_OK;
 }
 

@@ -202,6 +202,45 @@ def test_host_buffer_entry_matches_device(canny):
     assert np.array_equal(hl, _np(lab)) and np.array_equal(hf, _np(fin))
 
 
+@pytest.mark.parametrize("shape", [(5, 67, 131), (7, 33, 64), (1, 1, 3), (9, 120, 160)])
+def test_host_entry_packed_transfer_shapes(canny, shape):
+    """Host path ships (labels, final) packed to 2 bits/px and unpacks on the host:
+    odd pixel counts, chunk tails and single pixels must round-trip exactly."""
+    rng = np.random.default_rng(sum(shape))
+    frames = rng.integers(0, 256, size=shape, dtype=np.uint8)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    hl, hf = canny.canny_u8_host(frames, w, 20.0, 50.0)
+    assert np.array_equal(hl, _np(lab)) and np.array_equal(hf, _np(fin))
+
+
+def test_host_entry_pinned_pageable_and_misaligned_outputs(canny):
+    import torch
+    frames = synth.config3(6, 128)
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    lab, fin = _np(lab), _np(fin)
+    # pinned input
+    pin = torch.from_numpy(frames).pin_memory()
+    hl = np.empty(frames.shape, np.uint8)
+    hf = np.empty(frames.shape, np.uint8)
+    canny.canny_u8_host_ptr(pin.data_ptr(), *frames.shape, w, 20.0, 50.0, hl.ctypes.data, hf.ctypes.data)
+    assert np.array_equal(hl, lab) and np.array_equal(hf, fin)
+    # pageable input, outputs at different 16-byte phases
+    big_l = np.full(frames.size + 64, 7, np.uint8)
+    big_f = np.full(frames.size + 64, 7, np.uint8)
+    ol = big_l[3:3 + frames.size].reshape(frames.shape)
+    of = big_f[8:8 + frames.size].reshape(frames.shape)
+    canny.canny_u8_host_ptr(frames.ctypes.data, *frames.shape, w, 20.0, 50.0, ol.ctypes.data, of.ctypes.data)
+    assert np.array_equal(ol, lab) and np.array_equal(of, fin)
+    assert (big_l[:3] == 7).all() and (big_l[3 + frames.size:] == 7).all()
+    assert (big_f[:8] == 7).all() and (big_f[8 + frames.size:] == 7).all()
+    # device-resident "host" pointer (cudaMemcpyDefault path)
+    d = _dev(frames)
+    canny.canny_u8_host_ptr(d.data_ptr(), *frames.shape, w, 20.0, 50.0, hl.ctypes.data, hf.ctypes.data)
+    assert np.array_equal(hl, lab) and np.array_equal(hf, fin)
+
+
 def test_invalid_arguments_raise_valueerror(canny):
     w = O.gaussian_weights(1.4)
     img = _dev(np.zeros((8, 8), np.uint8))
