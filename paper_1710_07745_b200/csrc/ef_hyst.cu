@@ -30,15 +30,46 @@ constexpr int HP = 4 * HT;      // perimeter slots per tile
 constexpr int H_THREADS = 128;  // 32 pixels per thread: row = tid/2, columns 32*(tid%2) ..
 constexpr int NO_POS = 0xffff;  // fits the 16-bit minpos entries
 
+constexpr int LCAP = 256;           // listed foreground pixels per warp (16 rows x 64)
+constexpr unsigned NO_SLOT = 0x1ffu;  // info[] slot field: component touches no perimeter slot
+
 struct TileCCL {
     unsigned long long fgrow[HT];  // foreground (label != 0) bit per pixel, one word per row
     unsigned long long strow[HT];  // strong bit per pixel
-    unsigned short par[HT * HT];     // union-find parent; initialised for foreground pixels only
-    unsigned short minpos[HT * HT];  // smallest perimeter slot per root (foreground only)
-    unsigned char sflag[HT * HT];  // component holds a strong pixel (per root)
+    unsigned short par[HT * HT];   // union-find parent; initialised for foreground pixels only
+    // per root: bit 15 clear = component holds a strong pixel, bits 0..8 = its
+    // smallest perimeter slot (NO_SLOT if interior); 0xffff initially
+    unsigned short info[HT * HT];
+    unsigned short list[H_THREADS / 32][LCAP];  // each warp's foreground pixels (lane-balanced loops)
+    int wcount[H_THREADS / 32];
+    int flags;  // 1: any foreground, 2: any weak pixel, 4: a warp list overflowed
     int pending;
     int nodes;
 };
+
+__device__ __forceinline__ bool info_strong(unsigned v) { return !(v & 0x8000u); }
+__device__ __forceinline__ unsigned info_slot(unsigned v) { return v & NO_SLOT; }
+
+__device__ __forceinline__ void info_set_strong(unsigned short* p) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
+    atomicAnd(w, ~(0x8000u << sh));
+}
+
+// lower the slot field to v (CAS on the containing 32-bit word)
+__device__ __forceinline__ void info_min_slot(unsigned short* p, unsigned v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
+    unsigned int old = *w;
+    while (true) {
+        const unsigned cur = (old >> sh) & 0xffffu;
+        if ((cur & NO_SLOT) <= v) return;
+        const unsigned int nw = (old & ~(0xffffu << sh)) | (((cur & ~NO_SLOT) | v) << sh);
+        const unsigned int seen = atomicCAS(w, old, nw);
+        if (seen == old) return;
+        old = seen;
+    }
+}
 
 __device__ __forceinline__ int sfind(unsigned short* par, int i) {
     while (true) {
@@ -57,21 +88,6 @@ __device__ __forceinline__ void sunite(unsigned short* par, int a, int b) {
         if (a == b) return;
         if (a < b) { int t = a; a = b; b = t; }
         if (atomicCAS(&par[a], (unsigned short)a, (unsigned short)b) == (unsigned short)a) return;
-    }
-}
-
-// 16-bit atomic min by CAS on the containing 32-bit word (border pixels only)
-__device__ __forceinline__ void atomic_min_u16(unsigned short* p, unsigned short v) {
-    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
-    unsigned int old = *w;
-    while (true) {
-        const unsigned short cur = (unsigned short)(old >> sh);
-        if (cur <= v) return;
-        const unsigned int nw = (old & ~(0xffffu << sh)) | ((unsigned int)v << sh);
-        const unsigned int seen = atomicCAS(w, old, nw);
-        if (seen == old) return;
-        old = seen;
     }
 }
 
@@ -152,11 +168,13 @@ __device__ __forceinline__ void pack4(uint32_t w, uint32_t& fg, uint32_t& st) {
 }
 
 // Load this thread's 32 label bytes as foreground / strong bit masks and publish
-// the tile's row words.  Also initialises union-find state for its foreground
-// pixels (runs inside the 32-pixel segment pre-linked to their start).
+// the tile's row words and flags.  Also initialises union-find state for its
+// foreground pixels (runs inside the 32-pixel segment pre-linked to their
+// start) and appends them to the warp's pixel list.  The caller's barrier
+// makes everything visible.
 __device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g,
                                           TileCCL& s, uint32_t& fg, uint32_t& st) {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int row = tid >> 1, seg = (tid & 1) * 32;
     const uint8_t* src = labels + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
     uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -180,6 +198,17 @@ __device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, in
     }
     reinterpret_cast<uint32_t*>(&s.fgrow[row])[tid & 1] = fg;
     reinterpret_cast<uint32_t*>(&s.strow[row])[tid & 1] = st;
+    // warp-exclusive prefix of the foreground counts -> list positions
+    const int cnt = __popc(fg);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    const bool listed = total <= LCAP;
     uint32_t m = fg;
     while (m) {
         const int k = __ffs(m) - 1;
@@ -188,35 +217,93 @@ __device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, in
         const int start = below ? (32 - __clz(below)) : 0;  // start of k's run inside the segment
         const int i = row * HT + seg + k;
         s.par[i] = (unsigned short)(row * HT + seg + start);
-        s.minpos[i] = NO_POS;
-        s.sflag[i] = 0;
+        s.info[i] = 0xffffu;
+        if (listed) s.list[warp][off++] = (unsigned short)i;
+    }
+    const unsigned any_fg = __any_sync(0xffffffffu, fg != 0);
+    const unsigned any_weak = __any_sync(0xffffffffu, (fg & ~st) != 0);
+    if (lane == 0) {
+        s.wcount[warp] = total;
+        const int f = (any_fg ? 1 : 0) | (any_weak ? 2 : 0) | (listed ? 0 : 4);
+        if (f) atomicOr(&s.flags, f);
     }
 }
 
+// Unions of foreground pixel i = (row, x) with its W neighbour across a segment
+// seam (runs inside a segment are pre-linked) and its N / NW / NE neighbours.
+__device__ __forceinline__ void unite_up(TileCCL& s, int i) {
+    const int row = i >> 6, x = i & (HT - 1);
+    if ((x & 31) == 0 && x > 0 && ((s.fgrow[row] >> (x - 1)) & 1ull)) sunite(s.par, i, i - 1);
+    if (row > 0) {
+        const unsigned long long up = s.fgrow[row - 1];
+        if ((up >> x) & 1ull) {
+            sunite(s.par, i, i - HT);
+        } else {
+            if (x > 0 && ((up >> (x - 1)) & 1ull)) sunite(s.par, i, i - HT - 1);
+            if (x < HT - 1 && ((up >> (x + 1)) & 1ull)) sunite(s.par, i, i - HT + 1);
+        }
+    }
+}
+
+// Root bookkeeping for foreground pixel i whose root is r.
+__device__ __forceinline__ void note_root(TileCCL& s, const TileGeo& g, int i, int r) {
+    const int row = i >> 6, x = i & (HT - 1);
+    if ((s.strow[row] >> x) & 1ull) info_set_strong(&s.info[r]);
+    const int p = perim_slot(row, x, g.vh, g.vw);
+    if (p != NO_POS) info_min_slot(&s.info[r], (unsigned)p);
+}
+
 // General tile CCL (foreground holds weak pixels).  After return par[] holds
-// roots for every foreground pixel, sflag[root] marks strong components and
-// minpos[root] the smallest perimeter slot (NO_POS if interior).
-__device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t fg, uint32_t st) {
+// roots for every foreground pixel and info[root] the component's strong flag
+// and smallest perimeter slot.  `listed`: every warp's foreground fitted its
+// list, so the union / root loops run over the lists with all lanes busy (a
+// thin edge leaves most row segments with 0-2 pixels; per-thread loops would
+// idle most lanes); otherwise each thread walks its own 32-pixel segment.
+__device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t fg, uint32_t st, bool listed) {
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
-    // unions: W across segments, N / NW / NE from the row above (bit tests)
-    const unsigned long long up = row > 0 ? s.fgrow[row - 1] : 0ull;
-    const unsigned long long cur = s.fgrow[row];
+    constexpr int NW = H_THREADS / 32;
+    constexpr int RJ = NW * LCAP / H_THREADS;  // list entries per thread at most
+    if (listed) {
+        int base[NW + 1];
+        base[0] = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) base[w + 1] = base[w] + s.wcount[w];
+        const int n = base[NW];
+        auto entry = [&](int e) -> int {
+            int w = 0;
+#pragma unroll
+            for (int v = 1; v < NW; ++v) w += e >= base[v];
+            return s.list[w][e - base[w]];
+        };
+        for (int e = tid; e < n; e += H_THREADS) unite_up(s, entry(e));
+        __syncthreads();
+        unsigned short roots[RJ];
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) {
+            const int e = tid + j * H_THREADS;
+            if (e < n) {
+                const int i = entry(e);
+                const int r = sfind(s.par, i);
+                roots[j] = (unsigned short)r;
+                note_root(s, g, i, r);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) {
+            const int e = tid + j * H_THREADS;
+            if (e < n) s.par[entry(e)] = roots[j];
+        }
+        __syncthreads();
+        return;
+    }
     {
         uint32_t m = fg;
         while (m) {
             const int k = __ffs(m) - 1;
             m &= m - 1;
-            const int x = seg + k, i = row * HT + x;
-            if (k == 0 && x > 0 && ((cur >> (x - 1)) & 1ull)) sunite(s.par, i, i - 1);
-            if (up) {
-                if ((up >> x) & 1ull) {
-                    sunite(s.par, i, i - HT);
-                } else {
-                    if (x > 0 && ((up >> (x - 1)) & 1ull)) sunite(s.par, i, i - HT - 1);
-                    if (x < HT - 1 && ((up >> (x + 1)) & 1ull)) sunite(s.par, i, i - HT + 1);
-                }
-            }
+            unite_up(s, row * HT + seg + k);
         }
     }
     __syncthreads();
@@ -227,12 +314,10 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
         while (m) {
             const int k = __ffs(m) - 1;
             m &= m - 1;
-            const int x = seg + k, i = row * HT + x;
+            const int i = row * HT + seg + k;
             const int r = sfind(s.par, i);
             roots[k] = r;
-            if ((st >> k) & 1u) s.sflag[r] = 1;
-            const int p = perim_slot(row, x, g.vh, g.vw);
-            if (p != NO_POS) atomic_min_u16(&s.minpos[r], (unsigned short)p);
+            note_root(s, g, i, r);
         }
     }
     __syncthreads();
@@ -273,26 +358,27 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
     const TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
-    if (tid == 0) { s.pending = 0; s.nodes = 0; }
+    if (tid == 0) { s.pending = 0; s.nodes = 0; s.flags = 0; }
+    __syncthreads();
     uint32_t fg, st;
     tile_load(labels, H, W, g, s, fg, st);
-    const int any_fg = __syncthreads_or(fg != 0);
-    int kind = 0;  // 0 empty, 1 strong-only, 2 general
+    __syncthreads();
+    const int flags = s.flags;
+    const int kind = (flags & 1) ? ((flags & 2) ? 2 : 1) : 0;  // 0 empty, 1 strong-only, 2 general
     uint32_t fin = 0;
-    if (any_fg) {
-        kind = __syncthreads_or((fg & ~st) != 0) ? 2 : 1;
+    if (kind) {
         if (kind == 1) {
             fin = fg;
         } else {
-            tile_ccl(g, s, fg, st);
+            tile_ccl(g, s, fg, st, !(flags & 4));
             uint32_t pend = 0;
             uint32_t m = fg;
             while (m) {
                 const int k = __ffs(m) - 1;
                 m &= m - 1;
-                const int root = s.par[row * HT + seg + k];
-                if (s.sflag[root]) fin |= 1u << k;
-                else if (s.minpos[root] != NO_POS) pend |= 1u << k;
+                const unsigned v = s.info[s.par[row * HT + seg + k]];
+                if (info_strong(v)) fin |= 1u << k;
+                else if (info_slot(v) != NO_SLOT) pend |= 1u << k;
             }
             if (pend) {
                 s.pending = 1;
@@ -309,7 +395,7 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                         pend &= pend - 1;
                         const int root = s.par[row * HT + seg + k];
                         b.plist_idx[at + j] = base + k;
-                        b.plist_node[at + j] = (int)(tile * HP) + s.minpos[root];
+                        b.plist_node[at + j] = (int)(tile * HP) + (int)info_slot(s.info[root]);
                         ++j;
                     }
                 }
@@ -336,11 +422,11 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                     atomicAdd(&s.nodes, 1);
                 }
             } else {
-                const int root = s.par[y * HT + x];
-                node = (int)(tile * HP) + s.minpos[root];
-                if (s.minpos[root] == p) {
+                const unsigned v = s.info[s.par[y * HT + x]];
+                node = (int)(tile * HP) + (int)info_slot(v);
+                if (info_slot(v) == (unsigned)p) {
                     b.gpar[node] = node;
-                    b.gstrong[node] = s.sflag[root];
+                    b.gstrong[node] = info_strong(v) ? 1 : 0;
                     atomicAdd(&s.nodes, 1);
                 }
             }
@@ -476,10 +562,12 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
     const int txi = (int)(tile % tiles_x);
     const long long rest = tile / tiles_x;
     const TileGeo g = tile_geo_xyz(txi, (int)(rest % tiles_y), (int)(rest / tiles_y), H, W);
+    if (threadIdx.x == 0) s.flags = 0;
+    __syncthreads();
     uint32_t fg, st;
     tile_load(labels, H, W, g, s, fg, st);
     __syncthreads();
-    tile_ccl(g, s, fg, st);
+    tile_ccl(g, s, fg, st, !(s.flags & 4));
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
     uint8_t* out = final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
@@ -487,9 +575,9 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
     while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
-        const int root = s.par[row * HT + seg + k];
-        if (s.sflag[root] || s.minpos[root] == NO_POS) continue;
-        const int node = (int)(tile * HP) + s.minpos[root];
+        const unsigned v = s.info[s.par[row * HT + seg + k]];
+        if (info_strong(v) || info_slot(v) == NO_SLOT) continue;
+        const int node = (int)(tile * HP) + (int)info_slot(v);
         if (b.gstrong[gfind_ro(b.gpar, node)]) out[k] = 1;
     }
     __syncthreads();  // shared state is reused by the next tile of this block
