@@ -299,21 +299,24 @@ def run_ours(args):
     sptr = int(st.cuda_stream)
 
     def step(i, ev=None):
+        # one fused ef_canny_u8 call; the library records `ev` right before the
+        # classifier kernel and right after its fix-up launches (same stream)
         src = srcs[i % nbuf]
         if ev is not None:
-            ev[0].record(st)
-        rc = lib.ef_classify_u8(src.data_ptr(), b, h, wd, wp, r, float(low), float(high), labels.data_ptr(),
-                                ws.data_ptr(), ws.numel(), sptr)
-        _lib.check(rc, "classify")
+            _lib.check(lib.ef_set_classify_events(ev[0].cuda_event, ev[1].cuda_event), "events")
+        rc = lib.ef_canny_u8(src.data_ptr(), b, h, wd, wp, r, float(low), float(high), labels.data_ptr(),
+                             final.data_ptr(), ws.data_ptr(), ws.numel(), sptr)
+        _lib.check(rc, "canny")
         if ev is not None:
-            ev[1].record(st)
-        rc = lib.ef_trace_edges(labels.data_ptr(), b, h, wd, final.data_ptr(), ws.data_ptr(), ws.numel(), sptr)
-        _lib.check(rc, "trace")
+            _lib.check(lib.ef_set_classify_events(None, None), "events")
 
     for i in range(args.warmup):
         step(i)
     canny.reset_stats(ws)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, c in evs:  # torch creates the CUDA event on first record
+        a.record(st)
+        c.record(st)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()

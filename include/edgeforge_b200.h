@@ -68,6 +68,12 @@ int ef_reset_stats(void* d_workspace, size_t workspace_bytes, void* stream);
 /* Synchronise `stream` and copy the statistics out. */
 int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream, ef_stats* h_out);
 
+/* Instrumentation (no reference counterpart): CUDA events (cudaEvent_t, or
+ * NULL to stop) that this thread's later classify launches -- ef_classify_u8,
+ * ef_canny_u8, ef_band_canny_u8 -- record on their stream right before the
+ * classifier kernel and right after its fix-up kernels. */
+int ef_set_classify_events(void* start_event, void* stop_event);
+
 /* Whole Canny path for u8 frames on the device -- replaces run_pipeline
  * (bench.py:61-126, operator="canny", explicit Thresholds) for inputs whose
  * pixels are integers in [0,255] (GrayImage holds them as float64, image.py:23-50).

@@ -38,6 +38,7 @@ _SIGNATURES = {
     "ef_workspace_bytes": ([I64, I32, I32], SZ),
     "ef_reset_stats": ([P, SZ, P], ctypes.c_int),
     "ef_read_stats": ([P, SZ, P, ctypes.POINTER(EfStats)], ctypes.c_int),
+    "ef_set_classify_events": ([P, P], ctypes.c_int),
     "ef_canny_u8": ([P, I64, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
     "ef_canny_f64": ([P, I64, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
     "ef_classify_u8": ([P, I64, I32, I32, P, I32, D, D, P, P, SZ, P], ctypes.c_int),
@@ -69,7 +70,8 @@ def load():
         from . import build as _build
 
         _build.build()
-    lib = ctypes.CDLL(LIB_PATH)
+    path = os.environ.get("EF_LIB_OVERRIDE", LIB_PATH)  # experiment builds (tools/); default in-tree
+    lib = ctypes.CDLL(path)
     for name, (args, res) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args

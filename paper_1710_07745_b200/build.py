@@ -16,12 +16,12 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libedgeforge_b200.so")
+OBJ = os.environ.get("EF_BUILD_OBJ", os.path.join(HERE, "_build"))  # overrides: experiment variants
+LIB = os.environ.get("EF_BUILD_OUT", os.path.join(HERE, "libedgeforge_b200.so"))
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE] + os.environ.get("EF_NVCC_EXTRA", "").split()
 
 
 def _sources():

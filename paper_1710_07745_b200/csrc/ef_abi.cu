@@ -57,8 +57,9 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
-    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, node_list, total;
-    unsigned long long fix_cap, plist_cap, node_cap;
+    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, plist_count, node_list, node_count,
+        pend_tiles, dense, fgbits, stbits, plane_bytes, total;
+    unsigned long long fix_cap, plist_scap, node_scap;
     HystLayout hl;
 };
 
@@ -80,14 +81,27 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     off = align_up(off + (size_t)L.hl.slots);
     L.pending = off;
     off = align_up(off + (size_t)L.hl.tiles);
-    L.plist_cap = std::max<unsigned long long>(1ull << 16, npx / 64);
+    L.plist_scap = std::max<unsigned long long>(1ull << 10, npx / 64 / PL_STRIPES);
     L.plist_idx = off;
-    off = align_up(off + L.plist_cap * sizeof(unsigned long long));
+    off = align_up(off + L.plist_scap * PL_STRIPES * sizeof(unsigned long long));
     L.plist_node = off;
-    off = align_up(off + L.plist_cap * sizeof(int));
-    L.node_cap = std::max<unsigned long long>(1ull << 16, (unsigned long long)L.hl.slots / 8);
+    off = align_up(off + L.plist_scap * PL_STRIPES * sizeof(int));
+    L.plist_count = off;
+    off = align_up(off + PL_STRIPES * sizeof(unsigned long long));
+    L.node_scap = std::max<unsigned long long>(1ull << 10, (unsigned long long)L.hl.slots / 8 / PL_STRIPES);
     L.node_list = off;
-    off = align_up(off + L.node_cap * sizeof(int));
+    off = align_up(off + L.node_scap * PL_STRIPES * sizeof(int));
+    L.node_count = off;
+    off = align_up(off + PL_STRIPES * sizeof(unsigned long long));
+    L.pend_tiles = off;
+    off = align_up(off + PL_STRIPES * sizeof(unsigned long long));
+    L.dense = off;
+    off = align_up(off + (size_t)L.hl.tiles * sizeof(int));
+    L.plane_bytes = (size_t)batch * H * ((W + 63) / 64) * sizeof(unsigned long long);
+    L.fgbits = off;
+    off = align_up(off + L.plane_bytes);
+    L.stbits = off;
+    off = align_up(off + L.plane_bytes);
     L.total = off;
     return L;
 }
@@ -96,6 +110,8 @@ struct Ws {
     WsHeader* hdr;
     unsigned long long* fix;
     HystBufs hb;
+    unsigned long long* fgbits;
+    unsigned long long* stbits;
 };
 
 Ws ws_bind(void* base, const WsLayout& L) {
@@ -109,20 +125,32 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.pending = reinterpret_cast<uint8_t*>(p + L.pending);
     w.hb.plist_idx = reinterpret_cast<unsigned long long*>(p + L.plist_idx);
     w.hb.plist_node = reinterpret_cast<int*>(p + L.plist_node);
-    w.hb.plist_cap = L.plist_cap;
+    w.hb.plist_count = reinterpret_cast<unsigned long long*>(p + L.plist_count);
+    w.hb.plist_scap = L.plist_scap;
     w.hb.node_list = reinterpret_cast<int*>(p + L.node_list);
-    w.hb.node_cap = L.node_cap;
+    w.hb.node_count = reinterpret_cast<unsigned long long*>(p + L.node_count);
+    w.hb.node_scap = L.node_scap;
+    w.hb.pend_tiles = reinterpret_cast<unsigned long long*>(p + L.pend_tiles);
+    w.hb.dense = reinterpret_cast<int*>(p + L.dense);
+    w.fgbits = reinterpret_cast<unsigned long long*>(p + L.fgbits);
+    w.stbits = reinterpret_cast<unsigned long long*>(p + L.stbits);
     return w;
 }
 
-__global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap) {
-    hdr->fix_count = 0;
-    hdr->fix_cap = cap;
-    hdr->overflow = 0;
-    hdr->plist_count = 0;
-    hdr->plist_overflow = 0;
-    hdr->node_count = 0;
-    hdr->node_overflow = 0;
+__global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs hb) {
+    if (threadIdx.x == 0) {
+        hdr->fix_count = 0;
+        hdr->fix_cap = cap;
+        hdr->overflow = 0;
+        hdr->plist_overflow = 0;
+        hdr->dense_count = 0;
+        hdr->node_overflow = 0;
+    }
+    if (threadIdx.x < PL_STRIPES) {
+        hb.plist_count[threadIdx.x] = 0;
+        hb.node_count[threadIdx.x] = 0;
+        hb.pend_tiles[threadIdx.x] = 0;
+    }
 }
 
 __global__ void ws_reset_stats_kernel(WsHeader* hdr) {
@@ -207,16 +235,31 @@ FastParams make_fast(const double* w, int r, double low, double high) {
 
 FrameGeom frame_geom(int H, int W) { return FrameGeom{H, W, 0, H, 0, H}; }
 
+// ef_set_classify_events: events this thread's classify launches record around
+// the classifier + fix-up kernels (bench.py's roofline timing).
+struct Timing {
+    cudaEvent_t start = nullptr, stop = nullptr;
+};
+Timing& timing() {
+    thread_local Timing t;
+    return t;
+}
+
 bool has_negative(const double* w, int r) {
     for (int i = 0; i <= 2 * r; ++i)
         if (w[i] < 0.0) return true;
     return false;
 }
 
+// fin != nullptr (fused pipeline): where the production classifier runs, it
+// also fills the workspace's foreground bit planes, fin is zeroed for the
+// hysteresis to write only final pixels, and *bits describes the planes
+// (bits->fg == nullptr otherwise).
 int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const double* w, int r,
                     double low, double high, uint8_t* labels, const Ws& ws, const WsLayout& L,
-                    cudaStream_t st) {
+                    cudaStream_t st, uint8_t* fin = nullptr, FgBits* bits = nullptr) {
     int sms = sm_count_current();
+    if (bits) *bits = FgBits{};
     if (has_negative(w, r)) {
         // the certified bounds assume a convex (non-negative) kernel; a signed
         // kernel takes the exact float64 kernel instead
@@ -227,25 +270,40 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
                  "exact kernel");
         return EF_OK;
     }
-    ws_begin_kernel<<<1, 1, 0, st>>>(ws.hdr, L.fix_cap);
+    ws_begin_kernel<<<1, PL_STRIPES, 0, st>>>(ws.hdr, L.fix_cap, ws.hb);
     EF_CHECK(cudaGetLastError(), "ws_begin");
     FastParams FP = make_fast(w, r, low, high);
-    EF_CHECK(launch_k1(src, batch, g, FP, labels, ws.fix, ws.hdr, st), "classify kernel");
+    FgBits B{};
+    static const bool no_bits = getenv("EF_NO_FG_BITS") != nullptr;  // A/B switch for profiling
+    if (fin && bits && !no_bits && k1_emits_bits(FP, g)) {
+        const int words = (g.W + 63) / 64;
+        B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)g.rows * words};
+        const size_t plane = (size_t)batch * g.rows * words * sizeof(unsigned long long);
+        EF_CHECK(cudaMemsetAsync(ws.fgbits, 0, plane, st), "bit planes");
+        EF_CHECK(cudaMemsetAsync(ws.stbits, 0, plane, st), "bit planes");
+        EF_CHECK(cudaMemsetAsync(fin, 0, (size_t)batch * g.rows * g.W, st), "final");
+        *bits = B;
+    }
+    const Timing& T = timing();
+    if (T.start) EF_CHECK(cudaEventRecord(T.start, st), "timing event");
+    EF_CHECK(launch_k1(src, batch, g, FP, labels, ws.fix, ws.hdr, B, st), "classify kernel");
     ExactParams XP = make_exact(w, r, low, high);
-    EF_CHECK(launch_fix(src, batch, g, XP, labels, ws.fix, ws.hdr, sms, st), "fix-up kernel");
+    EF_CHECK(launch_fix(src, batch, g, XP, labels, ws.fix, ws.hdr, B, sms, st), "fix-up kernel");
+    if (T.stop) EF_CHECK(cudaEventRecord(T.stop, st), "timing event");
     return EF_OK;
 }
 
 // reset: the workspace header has not been initialised by a classify launch of
 // this call (standalone tracing).
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
-              cudaStream_t st, bool finalize, bool reset) {
+              cudaStream_t st, bool finalize, bool reset, const FgBits* bits = nullptr) {
     const int sms = sm_count_current();
     if (reset) {
-        ws_begin_kernel<<<1, 1, 0, st>>>(ws.hdr, L.fix_cap);
+        ws_begin_kernel<<<1, PL_STRIPES, 0, st>>>(ws.hdr, L.fix_cap, ws.hb);
         EF_CHECK(cudaGetLastError(), "ws_begin");
     }
-    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis");
+    if (bits && !bits->fg) bits = nullptr;
+    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, bits, sms, st), "hysteresis");
     if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
     return EF_OK;
 }
@@ -308,10 +366,17 @@ int ef_canny_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t wid
     if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
     Ws ws = ws_bind(d_workspace, L);
     cudaStream_t st = (cudaStream_t)stream;
+    FgBits bits;
     if ((rc = run_classify_u8(d_src, batch, frame_geom(height, width), h_weights, radius, low, high, d_labels,
-                              ws, L, st)))
+                              ws, L, st, d_final, &bits)))
         return rc;
-    return run_trace(d_labels, batch, height, width, d_final, ws, L, st, true, false);
+    return run_trace(d_labels, batch, height, width, d_final, ws, L, st, true, false, &bits);
+}
+
+int ef_set_classify_events(void* start_event, void* stop_event) {
+    timing().start = static_cast<cudaEvent_t>(start_event);
+    timing().stop = static_cast<cudaEvent_t>(stop_event);
+    return EF_OK;
 }
 
 int ef_canny_f64(const double* d_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
@@ -712,8 +777,10 @@ int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t f
     const int ht = std::min(row0, halo), hb = std::min(full_height - row0 - rows, halo);
     FrameGeom g{ht + rows + hb, width, row0 - ht, full_height, row0, rows};
     cudaStream_t st = (cudaStream_t)stream;
-    if ((rc = run_classify_u8(d_src, 1, g, h_weights, radius, low, high, d_labels, ws, L, st))) return rc;
-    return run_trace(d_labels, 1, rows, width, d_final, ws, L, st, false, false);
+    FgBits bits;
+    if ((rc = run_classify_u8(d_src, 1, g, h_weights, radius, low, high, d_labels, ws, L, st, d_final, &bits)))
+        return rc;
+    return run_trace(d_labels, 1, rows, width, d_final, ws, L, st, false, false, &bits);
 }
 
 int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,

@@ -44,12 +44,11 @@ struct WsHeader {
     ef_stats stats;          // accumulated counters
     unsigned long long fix_count;
     unsigned long long fix_cap;
-    unsigned long long plist_count;  // hysteresis pending-pixel list (H1 -> H4)
-    unsigned long long node_count;   // hysteresis node list (H1 -> H3)
     unsigned int overflow;           // fix list overflowed: fix-up kernel scans all pixels
-    unsigned int plist_overflow;     // pending list overflowed: H4 re-runs tile CCL
-    unsigned int node_overflow;      // node list overflowed: H3 scans every perimeter slot
-    unsigned int pad[3];
+    unsigned int plist_overflow;     // a pending-list stripe overflowed: H4 re-runs tile CCL
+    unsigned int dense_count;        // tiles H1's warp kernel handed to the block kernel
+    unsigned int node_overflow;      // a node-list stripe overflowed: H3 scans every perimeter slot
+    unsigned int pad[4];
 };
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

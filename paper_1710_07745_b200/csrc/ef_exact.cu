@@ -208,9 +208,18 @@ __device__ __forceinline__ void out_coords(unsigned long long idx, const FrameGe
     y = g.out0 + yo;
 }
 
+// the fused pipeline's foreground bit planes for a fixed pixel
+__device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, unsigned long long f, int y, int x,
+                                         uint8_t lab) {
+    if (!B.fg || (threadIdx.x & 31) != 0 || (lab != 1 && lab != 2)) return;
+    const unsigned long long w = f * B.frame_words + (unsigned long long)(y - g.out0) * B.words + (unsigned)(x >> 6);
+    atomicOr(&B.fg[w], 1ull << (x & 63));
+    if (lab == 2) atomicOr(&B.st[w], 1ull << (x & 63));
+}
+
 __global__ void __launch_bounds__(FX_WARPS * 32)
 fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uint8_t* labels,
-                const unsigned long long* __restrict__ list, WsHeader* hdr) {
+                const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
     const int warp = threadIdx.x >> 5;
@@ -223,6 +232,7 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
         out_coords(idx, g, f, y, x);
         fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
                        labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
+        fix_bits(B, g, f, y, x, labels[idx]);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)&hdr->stats.fixups, hdr->fix_count);
 }
@@ -230,7 +240,7 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
 // Overflow path: the fix list was too small; scan every label byte.
 __global__ void __launch_bounds__(FX_WARPS * 32)
 fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P,
-                uint8_t* labels, WsHeader* hdr) {
+                uint8_t* labels, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
     if (!hdr->overflow) return;
@@ -249,6 +259,7 @@ fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, Exa
             out_coords(p, g, f, y, x);
             fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
                            labels + p, (unsigned long long*)&hdr->stats.ambiguous);
+            fix_bits(B, g, f, y, x, labels[p]);
         }
     }
 }
@@ -279,12 +290,12 @@ template cudaError_t launch_exact<double>(const double*, int64_t, int, int, cons
                                           double*, unsigned long long*, WsHeader*, cudaStream_t);
 
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
-                       uint8_t* labels, const unsigned long long* list, WsHeader* hdr, int sm_count,
-                       cudaStream_t st) {
-    fix_list_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, g, P, labels, list, hdr);
+                       uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
+                       int sm_count, cudaStream_t st) {
+    fix_list_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, g, P, labels, list, hdr, B);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fix_scan_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, batch, g, P, labels, hdr);
+    fix_scan_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, batch, g, P, labels, hdr, B);
     return cudaGetLastError();
 }
 

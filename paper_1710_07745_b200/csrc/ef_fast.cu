@@ -171,11 +171,16 @@ k1_classify_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, u
 }
 
 cudaError_t launch_k1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                      uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
-    if (k1v4_supported(P, g) && getenv("EF_K1_V4")) return launch_k1v4(src, batch, g, P, labels, fix_list, hdr, st);
-    if (k1v2_supported(P, g)) return launch_k1v2(src, batch, g, P, labels, fix_list, hdr, st);
+                      uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
+                      cudaStream_t st) {
+    if (k1v2_supported(P, g)) return launch_k1v2(src, batch, g, P, labels, fix_list, hdr, B, st);
     return launch_k1v1(src, batch, g, P, labels, fix_list, hdr, st);
 }
+
+// bit planes need the production classifier and a zero background class (it
+// writes bits for classified candidates only; with low == 0 every pixel is
+// foreground)
+bool k1_emits_bits(const FastParams& P, const FrameGeom& g) { return k1v2_supported(P, g) && P.cls0 == 0; }
 
 cudaError_t launch_k1v1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                         uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {

@@ -51,6 +51,13 @@ constexpr int V2_IN_ROWS = V2_BROWS + 2 * V2_MAXR;  // staged u8 input rows (TMA
 // staged box starts at xv0 & ~15 and is 16 columns wider than the tile.
 constexpr int V2_IN_COLS = V2_COLS + 16;
 
+struct V2Out {
+    uint8_t* labels;
+    unsigned long long out_base;
+    unsigned long long* fix_list;
+    WsHeader* hdr;
+};
+
 struct V2Smem {
     float b[V2_BROWS][V2_COLS];
     union {
@@ -59,6 +66,7 @@ struct V2Smem {
     };
     int q[V2_WARPS][QCAP];
     unsigned long long mbar;                           // TMA completion barrier
+    FgBits bits;  // the classifier's bit planes (bits.fg == nullptr: off); read by the out-of-line classifier
 };
 
 template <int R>
@@ -125,9 +133,9 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 // Rows of b computed per warp in phase 1: the tile's 68 b rows split 4 ways.
 constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 17
 
-template <int R, bool INTERIOR, bool STAGED>
+template <int R, bool INTERIOR, bool STAGED, class Smem>
 __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const FrameGeom& g, int xv0, int y0,
-                                          const FastParams& P, V2Smem& S, int warp, int lane) {
+                                          const FastParams& P, Smem& S, int warp, int lane) {
     constexpr int NR = V2Cfg<R>::NR;
     const int c = xv0 + 4 * lane;
     const int W = g.W;
@@ -237,27 +245,17 @@ struct V2Cls {
     int W, FH, out0;
 };
 
-struct V2Out {
-    uint8_t* labels;
-    unsigned long long out_base;
-    unsigned long long* fix_list;
-    WsHeader* hdr;
-};
 
 __device__ __forceinline__ int mslot(int Y) { return (Y + MRING) & (MRING - 1); }
 
-// Classify the 4 pixels of one queued group (certified; kFlag otherwise).
-template <int R>
-__device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0, int Yc, int cl, V2Smem& S,
-                                                  int warp, const V2Out O) {
-    const int W = P.W, FH = P.FH;
+// Classify the 4 pixels of one candidate group (certified; kFlag otherwise):
+// mu/mc/md are the squared-magnitude rows Yc-1, Yc, Yc+1 and bu/bm/bd the
+// blurred rows (clamped) of the tile, indexed by tile column.
+__device__ __forceinline__ void classify_group(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
+                                               const float* mc, const float* md, const float* bu, const float* bm,
+                                               const float* bd, const FgBits& bits, const V2Out& O) {
+    const int W = P.W;
     const float t1 = 0.41421356237309503f;
-    const float* mu = S.m[warp][mslot(Yc - 1)];
-    const float* mc = S.m[warp][mslot(Yc)];
-    const float* md = S.m[warp][mslot(Yc + 1)];
-    const float* bu = S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)];
-    const float* bm = S.b[Yc - (y0 - 2)];
-    const float* bd = S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)];
     uint32_t packed = 0;
     const int cc0 = 4 * cl;
     const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * W;
@@ -307,6 +305,22 @@ __device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0
         packed |= lab << (8 * k);
     }
     *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
+    if (bits.fg) {
+        // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
+        const uint32_t lo = packed & 0x03030303u;
+        const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;
+        const uint32_t stn = (((packed >> 1) & 0x01010101u) * 0x10204080u) >> 28;
+        if (fgn) fg_bits_or(bits, blockIdx.z, Yc - P.out0, xv0 + cc0, fgn, stn);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0, int Yc, int cl, V2Smem& S,
+                                                  int warp, const V2Out O) {
+    const int FH = P.FH;
+    classify_group(P, xv0, Yc, cl, S.m[warp][mslot(Yc - 1)], S.m[warp][mslot(Yc)], S.m[warp][mslot(Yc + 1)],
+                   S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)], S.b[Yc - (y0 - 2)],
+                   S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)], S.bits, O);
 }
 
 template <int R>
@@ -351,6 +365,7 @@ __device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, c
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, W, FH, g.out0};
     const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(Y0w - g.out0) * W + c);
+
     const int Wq = W >> 2;
     const int l = 4 * lane;
     const float* bp = &S.b[Y0w - 2 - (y0 - 2)][l];
@@ -448,11 +463,41 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// TMA: the u8 tile + halo (144 columns x TH+4+2R rows of frame z) lands in
+// shared memory in one bulk tensor copy; completion on an mbarrier.
+template <int R, class Smem>
+__device__ __forceinline__ void tma_stage(Smem& S, const CUtensorMap& tmap, int xv0, int y0, const FrameGeom& g) {
+    constexpr int rows = V2_BROWS + 2 * R;
+    const uint32_t bar = smem_u32(&S.mbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // init visible to the TMA unit
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * V2_IN_COLS)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+                "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
+                "r"(bar)
+            : "memory");
+    }
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar)
+            : "memory");
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(V2_THREADS, 6)
 k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
             unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
-            const __grid_constant__ CUtensorMap tmap, int use_tma) {
+            const __grid_constant__ CUtensorMap tmap, int use_tma, FgBits B) {
     extern __shared__ __align__(16) unsigned char smraw[];
     V2Smem& S = *reinterpret_cast<V2Smem*>(smraw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -461,37 +506,13 @@ k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     const int y0 = g.out0 + blockIdx.y * V2_TH;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
     V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
+    if (threadIdx.x == 0) S.bits = B;
     // interior tile: every column and row of the halo exists in the buffer and
     // every output row is classified -- no clamps, no predicated stores
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
     if (interior && use_tma) {
-        // TMA: the u8 tile + halo (128 columns x TH+4+2R rows of frame z) lands in
-        // shared memory in one bulk tensor copy; completion on an mbarrier.
-        constexpr int rows = V2_BROWS + 2 * R;
-        const uint32_t bar = smem_u32(&S.mbar);
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // init visible to the TMA unit
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * V2_IN_COLS)
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-                    "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
-                    "r"(bar)
-                : "memory");
-        }
-        uint32_t done = 0;
-        while (!done) {
-            asm volatile(
-                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                : "=r"(done)
-                : "r"(bar)
-                : "memory");
-        }
+        tma_stage<R>(S, tmap, xv0, y0, g);
         v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
         v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
@@ -504,6 +525,182 @@ k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         __syncthreads();
         v2_phase2<R, false>(g, xv0, y0, P, S, warp, lane, O);
     }
+}
+
+// ---------------------------------------------------------------------------
+// K1 v3: shared magnitude tile.  v2's warps each stream their own 8 output
+// rows with a private magnitude ring, so every warp recomputes 4 halo rows of
+// Sobel/magnitude (12 row steps per 8 rows).  Here the 4 warps split the 34
+// magnitude rows of the tile once (y0-1 .. y0+TH), write them to a shared
+// tile, record one candidate bit per 4-pixel group (the row's ballot), and
+// after one barrier classify the candidates with every lane busy.
+// ---------------------------------------------------------------------------
+constexpr int V3_MROWS = V2_TH + 2;                                   // magnitude rows y0-1 .. y0+TH
+constexpr int V3_MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;          // 9 per warp
+constexpr int V3_QCAP = 64;
+
+struct V3Smem {
+    float b[V2_BROWS][V2_COLS];
+    union {
+        float m[V3_MROWS][V2_COLS];                 // squared magnitudes
+        unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
+    };
+    unsigned cmask[V2_TH];                          // candidate groups per output row (bit = lane)
+    unsigned short q[V2_WARPS][V3_QCAP];            // per-warp compaction queue: row << 8 | group
+    unsigned long long mbar;
+    FgBits bits;
+};
+
+// d = b[x+1] - b[x-1] and s = b[x-1] + 2 b[x] + b[x+1] for this lane's 4 columns
+__device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], float (&sm)[4]) {
+    const float4 bb = *reinterpret_cast<const float4*>(brow);
+    // neighbour lanes' edge columns (lanes 0 / 31 get wrapped values: only
+    // columns no output depends on are affected)
+    const float bl = __shfl_up_sync(0xffffffffu, bb.w, 1);
+    const float br = __shfl_down_sync(0xffffffffu, bb.x, 1);
+    d[0] = bb.y - bl;
+    d[1] = bb.z - bb.x;
+    d[2] = bb.w - bb.y;
+    d[3] = br - bb.z;
+    sm[0] = fmaf(2.f, bb.x, bl + bb.y);
+    sm[1] = fmaf(2.f, bb.y, bb.x + bb.z);
+    sm[2] = fmaf(2.f, bb.z, bb.y + bb.w);
+    sm[3] = fmaf(2.f, bb.w, bb.z + br);
+}
+
+template <int R, bool INTERIOR>
+__device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, const FastParams& P, V3Smem& S,
+                                           int warp, int lane, const V2Out& O) {
+    constexpr int HXA = V2Cfg<R>::HXA;
+    constexpr int OW = V2Cfg<R>::OW;
+    const int W = g.W, FH = g.full_H;
+    const int j0 = warp * V3_MPW;  // this warp's magnitude rows j0 .. j0+8 (tile rows; Ym = y0 - 1 + j)
+    const int oy0 = g.out0, oy1 = g.out0 + g.rows;
+    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
+    const int c = xv0 + 4 * lane;
+    const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
+    const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
+    const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
+    const int l = 4 * lane;
+    const int Wq = W >> 2;
+    auto brow = [&](int Y) -> const float* {
+        return &S.b[(INTERIOR ? Y : clampi(Y, 0, FH - 1)) - (y0 - 2)][l];
+    };
+    uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
+    float d[3][4], sm[3][4];
+    sobel_row(brow(y0 - 2 + j0), d[0], sm[0]);
+    sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
+#pragma unroll
+    for (int u = 0; u < V3_MPW; ++u) {
+        const int j = j0 + u;
+        if (j >= V3_MROWS) break;  // warp-uniform (last warp has 7 rows)
+        const int Ym = y0 - 1 + j;
+        const int pu = u % 3, pm = (u + 1) % 3, pd = (u + 2) % 3;
+        sobel_row(brow(Ym + 1), d[pd], sm[pd]);
+        const float2 two = f2(2.f, 2.f);
+        const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[pd][0], d[pd][1])));
+        const float2 gx23 = fma2(two, f2(d[pm][2], d[pm][3]), add2(f2(d[pu][2], d[pu][3]), f2(d[pd][2], d[pd][3])));
+        const float2 gy01 = add2(f2(sm[pd][0], sm[pd][1]), f2(-sm[pu][0], -sm[pu][1]));
+        const float2 gy23 = add2(f2(sm[pd][2], sm[pd][3]), f2(-sm[pu][2], -sm[pu][3]));
+        float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
+        float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
+        if (edge) {
+            float m4[4] = {m01.x, m01.y, m23.x, m23.y};
+            edge_fix(m4, xv0, lane, W);
+            m01 = f2(m4[0], m4[1]);
+            m23 = f2(m4[2], m4[3]);
+        }
+        *reinterpret_cast<float4*>(&S.m[j][l]) = make_float4(m01.x, m01.y, m23.x, m23.y);
+        // output rows: candidate bits, and the background class for the rest
+        if (j >= 1 && j <= V2_TH) {
+            const bool row_ok = INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH);
+            bool cand = false;
+            if (out_lane && row_ok) {
+                cand = fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
+                if (!cand) *lab = fill;
+            }
+            const unsigned ballot = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) S.cmask[j - 1] = ballot;
+        }
+        lab += Wq;
+    }
+}
+
+template <int R>
+__device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
+                                         const V2Out O) {
+    const int FH = P.FH;
+    int qn = 0;
+    // rows warp, warp + 4, ...: compact the candidate groups, classify 32 at a time
+    for (int r = warp; r < V2_TH; r += V2_WARPS) {
+        const unsigned mask = S.cmask[r];
+        if ((mask >> lane) & 1u) S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 8) | lane);
+        qn += __popc(mask);
+        const bool last = r + V2_WARPS >= V2_TH;
+        while (qn >= 32 || (last && qn > 0)) {
+            __syncwarp();
+            const int take = min(qn, 32);
+            if (lane < take) {
+                const int e = S.q[warp][lane];
+                const int Yc = y0 + (e >> 8), cl = e & 255, j = e >> 8;  // m tile row of Yc is j + 1
+                classify_group(P, xv0, Yc, cl, S.m[j], S.m[j + 1], S.m[j + 2],
+                               S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)], S.b[Yc - (y0 - 2)],
+                               S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)], S.bits, O);
+            }
+            __syncwarp();
+            const int rest = qn - take;
+            const unsigned short moved = lane < rest ? S.q[warp][32 + lane] : 0;
+            __syncwarp();
+            if (lane < rest) S.q[warp][lane] = moved;
+            qn = rest;
+        }
+        __syncwarp();
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(V2_THREADS, 6)
+k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
+            unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
+            const __grid_constant__ CUtensorMap tmap, int use_tma, FgBits B) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    V3Smem& S = *reinterpret_cast<V3Smem*>(smraw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = blockIdx.x * V2Cfg<R>::OW;
+    const int xv0 = x0 - V2Cfg<R>::HXA;
+    const int y0 = g.out0 + blockIdx.y * V2_TH;
+    const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
+    const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
+    if (threadIdx.x == 0) S.bits = B;
+    const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
+                          y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
+    if (interior) {
+        if (use_tma) {
+            tma_stage<R>(S, tmap, xv0, y0, g);
+            v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
+        } else {
+            v2_phase1<R, true, false>(img, g, xv0, y0, P, S, warp, lane);
+        }
+        __syncthreads();
+        v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
+        __syncthreads();
+    } else {
+        v2_phase1<R, false, false>(img, g, xv0, y0, P, S, warp, lane);
+        __syncthreads();
+        v3_phase2a<R, false>(g, xv0, y0, P, S, warp, lane, O);
+        __syncthreads();
+        // magnitude rows -1 and FH replicate rows 0 and FH-1 (np.pad edge)
+        const int FH = g.full_H;
+        if (y0 - 1 < 0 || y0 + V2_TH >= FH) {
+            const int t = threadIdx.x;  // 128 threads = one row of 128 columns
+            if (y0 - 1 < 0) S.m[0][t] = S.m[1][t];
+            const int jf = FH - (y0 - 1);  // tile row of Ym = FH
+            if (jf >= 1 && jf < V3_MROWS) S.m[jf][t] = S.m[jf - 1][t];
+            __syncthreads();
+        }
+    }
+    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
+    v3_classify<R>(CP, xv0, y0, S, warp, lane, O);
 }
 
 bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 6 && (g.W % 4) == 0; }
@@ -540,31 +737,35 @@ static bool make_src_map(CUtensorMap& tm, const uint8_t* src, int64_t batch, con
 
 template <int R>
 static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                            uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
-    const int smem = (int)sizeof(V2Smem);
-    cudaError_t e = cudaFuncSetAttribute(k1v2_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                            uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
+                            cudaStream_t st) {
+    static const bool v2 = getenv("EF_K1_V2") != nullptr;  // previous layout, for A/B runs
+    auto kern = v2 ? k1v2_kernel<R> : k1v3_kernel<R>;
+    const int smem = v2 ? (int)sizeof(V2Smem) : (int)sizeof(V3Smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     // occupancy is shared-memory bound: ask for the largest carveout
-    e = cudaFuncSetAttribute(k1v2_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     dim3 grid((g.W + V2Cfg<R>::OW - 1) / V2Cfg<R>::OW, (g.rows + V2_TH - 1) / V2_TH, (unsigned)batch);
     CUtensorMap tm;
     std::memset(&tm, 0, sizeof tm);
     const int use_tma = make_src_map(tm, src, batch, g, R) && !getenv("EF_NO_TMA");
-    k1v2_kernel<R><<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr, tm, use_tma);
+    kern<<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr, tm, use_tma, B);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k1v2(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st) {
+                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
+                        cudaStream_t st) {
     switch (P.r) {
-        case 1: return launch_r<1>(src, batch, g, P, labels, fix_list, hdr, st);
-        case 2: return launch_r<2>(src, batch, g, P, labels, fix_list, hdr, st);
-        case 3: return launch_r<3>(src, batch, g, P, labels, fix_list, hdr, st);
-        case 4: return launch_r<4>(src, batch, g, P, labels, fix_list, hdr, st);
-        case 5: return launch_r<5>(src, batch, g, P, labels, fix_list, hdr, st);
-        case 6: return launch_r<6>(src, batch, g, P, labels, fix_list, hdr, st);
+        case 1: return launch_r<1>(src, batch, g, P, labels, fix_list, hdr, B, st);
+        case 2: return launch_r<2>(src, batch, g, P, labels, fix_list, hdr, B, st);
+        case 3: return launch_r<3>(src, batch, g, P, labels, fix_list, hdr, B, st);
+        case 4: return launch_r<4>(src, batch, g, P, labels, fix_list, hdr, B, st);
+        case 5: return launch_r<5>(src, batch, g, P, labels, fix_list, hdr, B, st);
+        case 6: return launch_r<6>(src, batch, g, P, labels, fix_list, hdr, B, st);
         default: return cudaErrorInvalidValue;
     }
 }

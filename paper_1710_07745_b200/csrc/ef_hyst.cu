@@ -44,7 +44,6 @@ struct TileCCL {
     int wcount[H_THREADS / 32];
     int flags;  // 1: any foreground, 2: any weak pixel, 4: a warp list overflowed
     int pending;
-    int nodes;
 };
 
 __device__ __forceinline__ bool info_strong(unsigned v) { return !(v & 0x8000u); }
@@ -350,15 +349,20 @@ __device__ __forceinline__ void store32(uint8_t* dst, int valid, uint32_t bits) 
 // own strong node (no union-find: anything touching them is strong anyway);
 // other tiles run the shared-memory union-find and append the pixels of
 // undecided border components to the pending list for H4.
-__global__ void __launch_bounds__(H_THREADS)
-hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
-                  uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
-    __shared__ TileCCL s;
-    const long long tile = tile_id_xyz(tiles_x, tiles_y);
-    const TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
+// one border-component node into the node list stripe of its tile
+__device__ __forceinline__ void append_node(const HystBufs& b, WsHeader* hdr, long long tile, int node) {
+    const int stripe = (int)(tile % PL_STRIPES);
+    const unsigned long long at = atomicAdd(&b.node_count[stripe], 1ull);
+    if (at < b.node_scap) b.node_list[(unsigned long long)stripe * b.node_scap + at] = node;
+    else hdr->node_overflow = 1u;
+}
+
+__device__ __forceinline__ void hyst_block_tile(const uint8_t* __restrict__ labels, int H, int W,
+                                                uint8_t* __restrict__ final_out, const HystBufs& b, WsHeader* hdr,
+                                                long long tile, const TileGeo& g, TileCCL& s) {
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
-    if (tid == 0) { s.pending = 0; s.nodes = 0; s.flags = 0; }
+    if (tid == 0) { s.pending = 0; s.flags = 0; }
     __syncthreads();
     uint32_t fg, st;
     tile_load(labels, H, W, g, s, fg, st);
@@ -383,10 +387,12 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
             if (pend) {
                 s.pending = 1;
                 const int cnt = __popc(pend);
-                const unsigned long long at = atomicAdd(&hdr->plist_count, (unsigned long long)cnt);
-                if (at + cnt > b.plist_cap) {
+                const int stripe = (int)(tile % PL_STRIPES);
+                unsigned long long at = atomicAdd(&b.plist_count[stripe], (unsigned long long)cnt);
+                if (at + cnt > b.plist_scap) {
                     hdr->plist_overflow = 1u;
                 } else {
+                    at += (unsigned long long)stripe * b.plist_scap;
                     const unsigned long long base =
                         (unsigned long long)g.f * H * W + (unsigned long long)(g.y0 + row) * W + g.x0 + seg;
                     int j = 0;
@@ -419,7 +425,7 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                 if (own == p) {
                     b.gpar[node] = node;
                     b.gstrong[node] = 1;
-                    atomicAdd(&s.nodes, 1);
+                    append_node(b, hdr, tile, node);
                 }
             } else {
                 const unsigned v = s.info[s.par[y * HT + x]];
@@ -427,35 +433,370 @@ hyst_local_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
                 if (info_slot(v) == (unsigned)p) {
                     b.gpar[node] = node;
                     b.gstrong[node] = info_strong(v) ? 1 : 0;
-                    atomicAdd(&s.nodes, 1);
+                    append_node(b, hdr, tile, node);
                 }
             }
         }
         b.perim[tile * HP + p] = node;
     }
-    __syncthreads();
-    // this tile's nodes are the slots with perim[slot] == own id; list them for H3
-    if (s.nodes) {
-        __shared__ unsigned long long nbase;
-        if (tid == 0) nbase = atomicAdd(&hdr->node_count, (unsigned long long)s.nodes);
-        __syncthreads();
-        if (nbase + s.nodes <= b.node_cap) {
-            __shared__ int ncur;
-            if (tid == 0) ncur = 0;
-            __syncthreads();
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int p = tid + h * H_THREADS;
-                if (b.perim[tile * HP + p] == (int)(tile * HP) + p) b.node_list[nbase + atomicAdd(&ncur, 1)] = (int)(tile * HP) + p;
-            }
-        } else if (tid == 0) {
-            hdr->node_overflow = 1u;
-        }
-    }
     if (tid == 0) {
         b.pending[tile] = (uint8_t)s.pending;
-        if (s.nodes) atomicAdd((unsigned long long*)&hdr->stats.border_nodes, (unsigned long long)s.nodes);
-        if (s.pending) atomicAdd((unsigned long long*)&hdr->stats.pending_tiles, 1ull);
+        if (s.pending) atomicAdd(&b.pend_tiles[tile % PL_STRIPES], 1ull);
+    }
+    __syncthreads();  // shared state is reused by the block's next tile
+}
+
+__device__ __forceinline__ TileGeo tile_geo_linear(long long tile, int tiles_x, int tiles_y, int H, int W) {
+    const int txi = (int)(tile % tiles_x);
+    const long long rest = tile / tiles_x;
+    return tile_geo_xyz(txi, (int)(rest % tiles_y), (int)(rest / tiles_y), H, W);
+}
+
+// H1 for the tiles the warp kernel handed over (more foreground than its
+// compact lists hold): one 128-thread block per tile.
+__global__ void __launch_bounds__(H_THREADS)
+hyst_dense_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+                  uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
+    __shared__ TileCCL s;
+    const unsigned n = hdr->dense_count;
+    for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
+        const long long tile = b.dense[e];
+        hyst_block_tile(labels, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// H1 (warp per tile).  Canny foreground is sparse (C1: ~1% of pixels, ~40 per
+// 64x64 tile, a third of the tiles empty), so a tile is one warp's work: row
+// bitmasks in shared memory, union-find over COMPACT foreground indices
+// (rank of the pixel among the tile's foreground in row-major order, from a
+// row prefix count and a popcount), no block barriers.  ~5 KB of shared
+// memory per tile instead of ~20 KB.  Tiles with more than WCAP foreground
+// pixels go to hyst_dense_kernel.
+// ---------------------------------------------------------------------------
+constexpr int WCAP = 512;
+constexpr int WT_WARPS = 4;  // tiles per block (small: a block holds its slot until its slowest tile ends)
+
+struct WarpTile {
+    unsigned long long fgrow[HT];
+    unsigned long long strow[HT];
+    unsigned long long finrow[HT];
+    unsigned short rowbase[HT + 1];
+    unsigned short par[WCAP];
+    unsigned short info[WCAP];  // as TileCCL::info, per compact index
+    unsigned short list[WCAP];  // compact index -> tile pixel (row * 64 + x)
+};
+
+__device__ __forceinline__ int cidx(const WarpTile& s, int r, int x) {
+    return s.rowbase[r] + __popcll(s.fgrow[r] & ((1ull << x) - 1ull));
+}
+
+__device__ __forceinline__ int wfind(const unsigned short* par, int i) {  // read-only
+    while (true) {
+        const int p = par[i];
+        if (p == i) return i;
+        i = p;
+    }
+}
+
+// 16 bits -> 16 bytes (0/1)
+__device__ __forceinline__ uint4 expand16(uint32_t bits) {
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = (((bits >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// k-th (0-based) set bit of m
+__device__ __forceinline__ int select64(unsigned long long m, int k) {
+    int pos = 0;
+    uint32_t v = (uint32_t)m;
+    int c = __popc(v);
+    if (k >= c) {
+        k -= c;
+        v = (uint32_t)(m >> 32);
+        pos = 32;
+    }
+    c = __popc(v & 0xffffu);
+    if (k >= c) { k -= c; v >>= 16; pos += 16; }
+    c = __popc(v & 0xffu);
+    if (k >= c) { k -= c; v >>= 8; pos += 8; }
+    c = __popc(v & 0xfu);
+    if (k >= c) { k -= c; v >>= 4; pos += 4; }
+    c = __popc(v & 0x3u);
+    if (k >= c) { k -= c; v >>= 2; pos += 2; }
+    return pos + (k >= (int)(v & 1u) ? 1 : 0);
+}
+
+// row holding compact index e (the largest row whose prefix count is <= e)
+__device__ __forceinline__ int row_of(const WarpTile& s, int e) {
+    int r = 0;
+#pragma unroll
+    for (int step = 32; step >= 1; step >>= 1)
+        if (s.rowbase[r + step] <= e) r += step;
+    return r;
+}
+
+// BITS: the fused pipeline -- the classifier ORed the foreground / strong
+// pixels into bit planes and final_out was zeroed, so a tile reads 2 bits per
+// pixel (no label bytes) and stores one byte per final pixel.  Otherwise the
+// label bytes are read and the whole final tile is written.
+// Grid: (ceil(tiles per frame / WT_WARPS), frames); one warp per tile.
+template <bool BITS>
+__global__ void __launch_bounds__(32 * WT_WARPS)
+hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+                       uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr, FgBits B) {
+    __shared__ WarpTile tiles[WT_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tpf = tiles_x * tiles_y;
+    const int t = blockIdx.x * WT_WARPS + warp;
+    if (t >= tpf) return;  // warp-uniform; no block barriers below
+    WarpTile& s = tiles[warp];
+    const int ty = t / tiles_x;
+    const TileGeo g = tile_geo_xyz(t - ty * tiles_x, ty, blockIdx.y, H, W);
+    const long long tile = (long long)blockIdx.y * tpf + t;
+    const int stripe = t % PL_STRIPES;  // == tile % PL_STRIPES only up to the frame offset: any stripe works
+    const size_t frame_off = (size_t)g.f * H * W;
+    const int q = lane & 3, rsub = lane >> 2;  // label path: 4 lanes per row, 16 bytes each
+    if (BITS) {
+        // rows 2*lane, 2*lane+1 of word column tx
+        const unsigned long long w0 =
+            (unsigned long long)g.f * B.frame_words + (unsigned long long)(g.y0 + 2 * lane) * B.words + g.txi;
+        const bool r0 = 2 * lane < g.vh, r1 = 2 * lane + 1 < g.vh;
+        s.fgrow[2 * lane] = r0 ? __ldg(B.fg + w0) : 0ull;
+        s.strow[2 * lane] = r0 ? __ldg(B.st + w0) : 0ull;
+        s.fgrow[2 * lane + 1] = r1 ? __ldg(B.fg + w0 + B.words) : 0ull;
+        s.strow[2 * lane + 1] = r1 ? __ldg(B.st + w0 + B.words) : 0ull;
+    } else {
+        // all eight 16-byte loads are issued before any is consumed (one DRAM
+        // round trip per tile, not eight)
+        const bool full_in = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(labels) & 15) == 0);
+        uint4 v[HT / 8];
+        const uint8_t* src0 = labels + frame_off + (size_t)(g.y0 + rsub) * W + g.x0 + 16 * q;
+#pragma unroll
+        for (int it = 0; it < HT / 8; ++it) {
+            const int r = it * 8 + rsub;
+            v[it] = make_uint4(0u, 0u, 0u, 0u);
+            if (r < g.vh) {
+                const uint8_t* src = src0 + (size_t)(it * 8) * W;
+                if (full_in) {
+                    v[it] = __ldg(reinterpret_cast<const uint4*>(src));
+                } else {
+                    uint32_t w4[4] = {0u, 0u, 0u, 0u};
+                    for (int k = 0; k < 16 && 16 * q + k < g.vw; ++k) w4[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
+                    v[it] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < HT / 8; ++it) {
+            const int r = it * 8 + rsub;
+            const uint32_t w4[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+            uint32_t f16 = 0, s16 = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t f, tt;
+                pack4(w4[j], f, tt);
+                f16 |= f << (4 * j);
+                s16 |= tt << (4 * j);
+            }
+            // gather the row's four quarters (lanes 4*rsub .. 4*rsub+3)
+            unsigned long long fr = (unsigned long long)f16 << (16 * q);
+            unsigned long long sr = (unsigned long long)s16 << (16 * q);
+            fr |= __shfl_xor_sync(0xffffffffu, fr, 1);
+            sr |= __shfl_xor_sync(0xffffffffu, sr, 1);
+            fr |= __shfl_xor_sync(0xffffffffu, fr, 2);
+            sr |= __shfl_xor_sync(0xffffffffu, sr, 2);
+            if (q == 0) {
+                s.fgrow[r] = fr;
+                s.strow[r] = sr;
+            }
+        }
+    }
+    __syncwarp();
+    // ---- each lane owns rows 2*lane, 2*lane+1 for the prefix counts
+    const unsigned long long f0 = s.fgrow[2 * lane], f1 = s.fgrow[2 * lane + 1];
+    const unsigned long long s0 = s.strow[2 * lane], s1 = s.strow[2 * lane + 1];
+    const bool any_fg = __any_sync(0xffffffffu, (f0 | f1) != 0ull);
+    const bool any_weak = __any_sync(0xffffffffu, ((f0 & ~s0) | (f1 & ~s1)) != 0ull);
+    const int c0 = __popcll(f0), c1 = __popcll(f1);
+    int incl = c0 + c1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const int n = __shfl_sync(0xffffffffu, incl, 31);
+    if (any_weak && n > WCAP) {  // dense tile: the block kernel takes it (reads the labels)
+        if (lane == 0) b.dense[atomicAdd(&hdr->dense_count, 1u)] = (int)tile;
+        return;
+    }
+    const int kind = any_fg ? (any_weak ? 2 : 1) : 0;  // empty, strong only, general
+    bool tile_pending = false;
+    if (kind) {
+        const int base0 = incl - c0 - c1;
+        s.rowbase[2 * lane] = (unsigned short)base0;
+        s.rowbase[2 * lane + 1] = (unsigned short)(base0 + c0);
+        if (lane == 31) s.rowbase[HT] = (unsigned short)n;
+        s.finrow[2 * lane] = 0ull;
+        s.finrow[2 * lane + 1] = 0ull;
+        __syncwarp();
+    }
+    auto store_final = [&](int r, int x) {
+        final_out[frame_off + (size_t)(g.y0 + r) * W + g.x0 + x] = 1;
+    };
+    if (kind == 1 && BITS) {
+        for (int e = lane; e < n; e += 32) {
+            const int r = row_of(s, e);
+            store_final(r, select64(s.fgrow[r], e - s.rowbase[r]));
+        }
+    }
+    if (kind == 2) {
+        // compact list + union-find init, lane-balanced: index e -> (row, column)
+        // by the prefix counts; runs are pre-linked to their start
+        for (int e = lane; e < n; e += 32) {
+            const int r = row_of(s, e);
+            const unsigned long long fr = s.fgrow[r];
+            const int x = select64(fr, e - s.rowbase[r]);
+            const unsigned long long below = ~fr & ((1ull << x) - 1ull);
+            const int start = below ? 64 - __clzll((long long)below) : 0;
+            s.list[e] = (unsigned short)(r * HT + x);
+            s.par[e] = (unsigned short)(e - (x - start));
+            s.info[e] = 0xffffu;
+        }
+        __syncwarp();
+        // unions with the row above
+        for (int e = lane; e < n; e += 32) {
+            const int pix = s.list[e];
+            const int r = pix >> 6, x = pix & (HT - 1);
+            if (r == 0) continue;
+            const unsigned long long up = s.fgrow[r - 1];
+            if ((up >> x) & 1ull) {
+                sunite(s.par, e, cidx(s, r - 1, x));
+            } else {
+                if (x > 0 && ((up >> (x - 1)) & 1ull)) sunite(s.par, e, cidx(s, r - 1, x - 1));
+                if (x < HT - 1 && ((up >> (x + 1)) & 1ull)) sunite(s.par, e, cidx(s, r - 1, x + 1));
+            }
+        }
+        __syncwarp();
+        // roots (read-only finds, so par[e] = root can be written at once) and
+        // per-component strong flag / smallest perimeter slot
+        for (int e = lane; e < n; e += 32) {
+            const int pix = s.list[e];
+            const int r = pix >> 6, x = pix & (HT - 1);
+            const int root = wfind(s.par, e);
+            s.par[e] = (unsigned short)root;
+            if ((s.strow[r] >> x) & 1ull) info_set_strong(&s.info[root]);
+            const int p = perim_slot(r, x, g.vh, g.vw);
+            if (p != NO_POS) info_min_slot(&s.info[root], (unsigned)p);
+        }
+        __syncwarp();
+        // final pixels; undecided border components -> pending list
+        for (int e0 = 0; e0 < n; e0 += 32) {
+            const int e = e0 + lane;
+            bool pend = false;
+            int pix = 0;
+            unsigned v = 0;
+            if (e < n) {
+                pix = s.list[e];
+                v = s.info[s.par[e]];
+                if (info_strong(v)) {
+                    if (BITS) store_final(pix >> 6, pix & (HT - 1));
+                    else atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
+                } else {
+                    pend = info_slot(v) != NO_SLOT;
+                }
+            }
+            const unsigned pb = __ballot_sync(0xffffffffu, pend);
+            if (pb) {
+                tile_pending = true;
+                unsigned long long at = 0;
+                if (lane == 0) at = atomicAdd(&b.plist_count[stripe], (unsigned long long)__popc(pb));
+                at = __shfl_sync(0xffffffffu, at, 0);
+                if (at + __popc(pb) > b.plist_scap) {
+                    if (lane == 0) hdr->plist_overflow = 1u;
+                } else if (pend) {
+                    const unsigned long long o =
+                        (unsigned long long)stripe * b.plist_scap + at + __popc(pb & ((1u << lane) - 1u));
+                    b.plist_idx[o] = frame_off + (unsigned long long)(g.y0 + (pix >> 6)) * W + g.x0 + (pix & (HT - 1));
+                    b.plist_node[o] = (int)(tile * HP) + (int)info_slot(v);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (!BITS) {
+        // ---- whole final tile (4 lanes per row, 16 bytes each)
+        const bool full_out = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(final_out) & 15) == 0);
+#pragma unroll 2
+        for (int it = 0; it < HT / 8; ++it) {
+            const int r = it * 8 + rsub;
+            if (r >= g.vh) continue;
+            const unsigned long long fr = kind == 2 ? s.finrow[r] : (kind == 1 ? s.fgrow[r] : 0ull);
+            const uint32_t bits = (uint32_t)(fr >> (16 * q)) & 0xffffu;
+            uint8_t* dst = final_out + frame_off + (size_t)(g.y0 + r) * W + g.x0 + 16 * q;
+            if (full_out) {
+                *reinterpret_cast<uint4*>(dst) = expand16(bits);
+            } else {
+                for (int k = 0; k < 16 && 16 * q + k < g.vw; ++k) dst[k] = (uint8_t)((bits >> k) & 1u);
+            }
+        }
+    }
+    // ---- perimeter slots (lane handles slots lane + 32 j): node id of the
+    // component at each slot; a component's own (smallest) slot makes it a node
+    int nodes[HP / 32];
+    unsigned own[HP / 32];
+    int total = 0;
+#pragma unroll
+    for (int j = 0; j < HP / 32; ++j) {
+        const int p = lane + 32 * j;
+        int y, x;
+        slot_pixel(p, g.vh, g.vw, y, x);
+        const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
+        int node = -1;
+        bool mine = false;
+        if (kind && valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
+            if (kind == 1) {
+                const int sl = perim_slot(y, x, g.vh, g.vw);
+                node = (int)(tile * HP) + sl;
+                if (sl == p) {
+                    mine = true;
+                    b.gpar[node] = node;
+                    b.gstrong[node] = 1;
+                }
+            } else {
+                const unsigned v = s.info[s.par[cidx(s, y, x)]];
+                node = (int)(tile * HP) + (int)info_slot(v);
+                if (info_slot(v) == (unsigned)p) {
+                    mine = true;
+                    b.gpar[node] = node;
+                    b.gstrong[node] = info_strong(v) ? 1 : 0;
+                }
+            }
+        }
+        b.perim[tile * HP + p] = node;
+        nodes[j] = node;
+        own[j] = __ballot_sync(0xffffffffu, mine);
+        total += __popc(own[j]);
+    }
+    if (total) {  // one append per tile into its node-list stripe
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(&b.node_count[stripe], (unsigned long long)total);
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (at + total > b.node_scap) {
+            if (lane == 0) hdr->node_overflow = 1u;
+        } else {
+            unsigned long long o = (unsigned long long)stripe * b.node_scap + at;
+#pragma unroll
+            for (int j = 0; j < HP / 32; ++j) {
+                if ((own[j] >> lane) & 1u) b.node_list[o + __popc(own[j] & ((1u << lane) - 1u))] = nodes[j];
+                o += __popc(own[j]);
+            }
+        }
+    }
+    if (lane == 0) {
+        b.pending[tile] = (uint8_t)tile_pending;
+        if (tile_pending) atomicAdd(&b.pend_tiles[stripe], 1ull);
     }
 }
 
@@ -510,21 +851,39 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, const int* __restrict_
     }
 }
 
-// H3: strong flag of every node onto its root (over H1's node list; every
-// perimeter slot if that list overflowed).
-__global__ void hyst_resolve_kernel(long long nslots, HystBufs b, const WsHeader* __restrict__ hdr) {
+// H3: strong flag of every node onto its root, over the node-list stripes
+// (every perimeter slot holding its own id if a stripe overflowed).  Block 0
+// also folds the per-stripe counts into the statistics.
+__global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr) {
     const bool all = hdr->node_overflow != 0;
-    const long long n = all ? nslots : (long long)hdr->node_count;
+    const long long n = all ? nslots : (long long)PL_STRIPES * (long long)b.node_scap;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         int node;
         if (all) {
             node = b.perim[e];
             if (node != (int)e) continue;  // the node's own (smallest) slot only
         } else {
+            const long long stripe = e / (long long)b.node_scap, k = e - stripe * (long long)b.node_scap;
+            if (k >= (long long)b.node_count[stripe]) continue;
             node = b.node_list[e];
         }
         const int r = gfind(b.gpar, node);
         if (b.gstrong[node] && r != node) b.gstrong[r] = 1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        unsigned long long nodes = 0, pend = 0;
+        for (int i = threadIdx.x; i < PL_STRIPES; i += 32) {
+            nodes += b.node_count[i];
+            pend += b.pend_tiles[i];
+        }
+        for (int d = 16; d; d >>= 1) {
+            nodes += __shfl_down_sync(0xffffffffu, nodes, d);
+            pend += __shfl_down_sync(0xffffffffu, pend, d);
+        }
+        if (threadIdx.x == 0) {
+            hdr->stats.border_nodes += nodes;
+            hdr->stats.pending_tiles += pend;
+        }
     }
 }
 
@@ -533,11 +892,13 @@ __global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs
     // on overflow the list is incomplete (chunks past the cap were dropped) and
     // hyst_final_tile_kernel finalises every pending tile instead
     if (hdr->plist_overflow) return;
-    unsigned long long n = hdr->plist_count;
-    if (n > b.plist_cap) n = b.plist_cap;
+    const unsigned long long n = (unsigned long long)PL_STRIPES * b.plist_scap;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-         e += (unsigned long long)gridDim.x * blockDim.x)
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long stripe = e / b.plist_scap, k = e - stripe * b.plist_scap;
+        if (k >= b.plist_count[stripe]) continue;
         if (b.gstrong[gfind_ro(b.gpar, b.plist_node[e])]) final_out[b.plist_idx[e]] = 1;
+    }
 }
 
 struct TileCCL;
@@ -624,15 +985,28 @@ HystLayout hyst_layout(int64_t batch, int H, int W) {
 }
 
 cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st) {
+                              const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
+                              cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
     const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
-    // ~21 KB of shared memory per tile: ask for the full carveout so ~10 tiles
-    // are resident per SM (the kernel is barrier/latency bound)
-    cudaFuncSetAttribute(hyst_local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(hyst_local_warp_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    hyst_local_kernel<<<tgrid, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
+    cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    // shared memory bound (5 KB per warp tile, 20 KB per dense tile): full carveout
+    cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    const dim3 wgrid((unsigned)((L.tiles_x * L.tiles_y + WT_WARPS - 1) / WT_WARPS), (unsigned)batch);
+    if (bits)
+        hyst_local_warp_kernel<true><<<wgrid, 32 * WT_WARPS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
+                                                                     b, hdr, *bits);
+    else
+        hyst_local_warp_kernel<false><<<wgrid, 32 * WT_WARPS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
+                                                                      b, hdr, FgBits{});
     cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    hyst_dense_kernel<<<sm_count * 4, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     hyst_merge_kernel<<<tgrid, 128, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b.perim, b.gpar);
     e = cudaGetLastError();

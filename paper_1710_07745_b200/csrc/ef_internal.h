@@ -25,17 +25,45 @@ struct HystLayout {
     int64_t tiles, slots;
 };
 
+constexpr int PL_STRIPES = 64;  // pending-list stripes (tile % 64): spreads the append counters
+
 struct HystBufs {
     int* perim;
     int* gpar;
     uint8_t* gstrong;
     uint8_t* pending;
-    unsigned long long* plist_idx;  // pixels of undecided border components (H1 -> H4)
-    int* plist_node;
-    unsigned long long plist_cap;
-    int* node_list;  // border-component node ids (H1 -> H3)
-    unsigned long long node_cap;
+    unsigned long long* plist_idx;  // pixels of undecided border components (H1 -> H4),
+    int* plist_node;                //   PL_STRIPES stripes of plist_scap entries
+    unsigned long long* plist_count;  // per stripe
+    unsigned long long plist_scap;
+    int* node_list;                  // border-component nodes (H1 -> H3), PL_STRIPES stripes of node_scap
+    unsigned long long* node_count;  // per stripe
+    unsigned long long node_scap;
+    unsigned long long* pend_tiles;  // per stripe: tiles with undecided border components (statistics)
+    int* dense;  // tiles too dense for the warp kernel (one entry per tile at most)
 };
+
+// Foreground bit planes for the fused pipeline (ef_canny_u8): the classifier
+// ORs every foreground / strong pixel into row-major bit planes (one bit per
+// pixel, 64-bit words), so hysteresis reads 2 bits per pixel instead of
+// rescanning the label bytes (about 1% of Canny labels are foreground).
+// fg == nullptr: planes off.
+struct FgBits {
+    unsigned long long* fg;
+    unsigned long long* st;
+    int words;                     // words per output row: ceil(W / 64)
+    unsigned long long frame_words;  // words per frame: rows * words
+};
+
+#ifdef __CUDACC__
+// pixels x .. x+3 (x % 4 == 0) of output row yo in frame f: nibbles of fg / strong bits
+__device__ __forceinline__ void fg_bits_or(const FgBits& B, unsigned long long f, int yo, int x, uint32_t fgn,
+                                           uint32_t stn) {
+    const unsigned long long w = f * B.frame_words + (unsigned long long)yo * B.words + (unsigned)(x >> 6);
+    if (fgn) atomicOr(&B.fg[w], (unsigned long long)fgn << (x & 63));
+    if (stn) atomicOr(&B.st[w], (unsigned long long)stn << (x & 63));
+}
+#endif
 
 size_t ex_smem_bytes(int r);
 size_t k1_smem_bytes(int r);
@@ -46,25 +74,29 @@ cudaError_t launch_exact(const In* src, int64_t batch, int H, int W, const Exact
                          int64_t* ori, double* thin, unsigned long long* max_bits, WsHeader* hdr,
                          cudaStream_t st);
 
+// B.fg != nullptr only where k1_emits_bits() holds
 cudaError_t launch_k1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                      uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
+                      uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
+                      cudaStream_t st);
+bool k1_emits_bits(const FastParams& P, const FrameGeom& g);
 
 cudaError_t launch_k1v1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                         uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
 cudaError_t launch_k1v2(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
+                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
+                        cudaStream_t st);
 bool k1v2_supported(const FastParams& P, const FrameGeom& g);
-cudaError_t launch_k1v4(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                        uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, cudaStream_t st);
-bool k1v4_supported(const FastParams& P, const FrameGeom& g);
 
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
-                       uint8_t* labels, const unsigned long long* list, WsHeader* hdr, int sm_count,
-                       cudaStream_t st);
+                       uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
+                       int sm_count, cudaStream_t st);
 
 HystLayout hyst_layout(int64_t batch, int H, int W);
+// bits: the classifier's foreground bit planes for these labels (final_out
+// zeroed beforehand), or nullptr to read the label bytes
 cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, WsHeader* hdr, int sm_count, cudaStream_t st);
+                              const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
+                              cudaStream_t st);
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st);
 cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,

@@ -109,6 +109,31 @@ def test_fast_path_random_vs_oracle(canny, r):
             assert np.array_equal(_np(fin)[0].astype(bool), ef_), (r, h, wd, kind, low, high)
 
 
+@pytest.mark.parametrize("density", ["sparse", "mixed", "dense"])
+def test_fused_foreground_lists_vs_two_call_path(canny, density):
+    """ef_canny_u8 builds per-tile foreground lists in the classifier (final
+    prefilled with the strong pixels); ef_classify_u8 + ef_trace_edges rescans
+    the labels.  Both must equal the oracle -- including tiles whose list
+    overflows (dense noise) and frames whose size is not a multiple of 64."""
+    rng = np.random.default_rng({"sparse": 1, "mixed": 2, "dense": 3}[density])
+    w = O.gaussian_weights(1.4, radius=2)
+    for (b, h, wd) in [(2, 130, 200), (1, 64, 128), (3, 97, 252)]:
+        if density == "sparse":
+            frames = synth.config1(b, h, wd)
+        elif density == "mixed":
+            frames = synth.config1(b, h, wd)
+            frames[:, : h // 2, : wd // 2] = rng.integers(0, 256, size=(b, h // 2, wd // 2), dtype=np.uint8)
+        else:
+            frames = rng.integers(0, 256, size=(b, h, wd), dtype=np.uint8)
+        lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+        lab2 = canny.classify_u8(_dev(frames), w, 20.0, 50.0)
+        fin2 = canny.trace_edges_u8(lab2)
+        el, ef_ = O.canny(frames, w, 20.0, 50.0)
+        assert np.array_equal(_np(lab), el) and np.array_equal(_np(lab2), el)
+        assert np.array_equal(_np(fin).astype(bool), ef_), (density, b, h, wd)
+        assert np.array_equal(_np(fin2).astype(bool), ef_), (density, b, h, wd)
+
+
 def test_float_path_random_vs_oracle(canny):
     rng = np.random.default_rng(5)
     for (h, wd) in [(1, 1), (7, 5), (33, 47), (128, 96)]:
