@@ -134,14 +134,14 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel_prefix="void k1v2_kernel"):
+def ncu_traffic(kernel_prefix="void k1v3_kernel"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
     kernel, from the committed ncu capture of this bench command
-    (profiles/r01_k1_dram_64frames.csv: `ncu --metrics ...dram__bytes_*...
+    (profiles/r01_k1v3_dram_64frames.csv: `ncu --metrics ...dram__bytes_*...
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`)."""
     import csv
 
-    path = os.path.join(ROOT, "profiles", "r01_k1_dram_64frames.csv")
+    path = os.path.join(ROOT, "profiles", "r01_k1v3_dram_64frames.csv")
     try:
         rows = list(csv.reader(open(path)))
     except OSError:
@@ -379,18 +379,18 @@ def run_ours(args):
                        "radius": args.radius, "sigma": 1.4, "thresholds": [low, high],
                        "parallelism": f"{world} independent batches (one per GPU)",
                        "l2": f"rotating {nbuf} resident input batches ({nbuf * px / 1e6:.0f} MB > 126 MB L2)"},
-            "roofline": {"bound": "hbm", "kernel": "k1_classify_kernel (+fix-up launches)",
+            "roofline": {"bound": "hbm", "kernel": "k1v3_kernel (+fix-up launches)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": ncu_traffic() if (args.config == 1 and b == 64 and args.radius == 2) else None,
-                         "traffic_source": "profiles/r01_k1_dram_64frames.csv (ncu dram__bytes_read+write per launch)",
+                         "traffic_source": "profiles/r01_k1v3_dram_64frames.csv (ncu dram__bytes_read+write per launch)",
                          "peak_kind": peak_kind,
                          "alg_bytes_per_launch": int(alg_bytes), "avg_launch_ms": round(k1_ms, 4),
                          "share_of_step": round(k1_ms / ms, 3)},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 8 * args.steps,
+            "gpu_launches": 10 * args.steps,  # ws_begin, K1, 2 fix-up, 2 H1, merge, resolve, 2 finalize
             "stats": {k: int(v) for k, v in stats.items()},
         }
         print(json.dumps(line), flush=True)

@@ -1,29 +1,33 @@
-// ef_fast2.cu -- K1 v2: the fused classify kernel, warp-streaming layout.
+// ef_fast2.cu -- K1: the fused classify kernel (production path for
+// radius 1..6 and W % 4 == 0; ef_fast.cu's v1 covers the rest).
 //
-// Same contract as ef_fast.cu (certified fp32 decisions, kFlag + fix list
-// for the rest); different structure, built for instruction economy:
+// Certified fp32 decisions with kFlag + fix list for the rest (the contract of
+// ef_fast.cu).  One CTA = 4 warps = a tile of 128 computed columns (32 lanes x
+// 4 adjacent columns) x TH = 32 output rows; OW = 128 - 2*HXA output columns
+// (HXA column halo each side: 4 for radius <= 2, 8 for radius <= 6).
 //
-//  tile      128 computed columns (32 lanes x 4 adjacent columns per lane) x
-//            64 output rows; OW = 128 - 2*HXA output columns (HXA column
-//            halo on each side, 4 for radius <= 2, 8 for radius <= 4).
-//  phase 1   each warp streams down a block of rows: one coalesced 4-byte
-//            load per lane per input row (prefetched 2R rows ahead), u8 ->
-//            fp32 by byte-permute + one FADD, vertical blur from a register
-//            ring of the last 2R+1 rows, horizontal blur with the neighbour
-//            lanes' columns from warp shuffles.  The blurred rows land in
-//            shared memory (b tile: 68 x 128 fp32).
-//  phase 2   each warp streams 16 output rows: Sobel from the b tile (period-3
-//            register rings of the row differences/sums), magnitude, and a
-//            per-warp 8-row ring of magnitudes in shared memory.  Pixels
-//            certainly below `low` (most of them) are written as the
-//            suppressed class right away; 4-pixel groups holding a possible
-//            edge go to a per-warp queue and are classified 32 at a time
-//            with every lane busy (sector, NMS, thresholds, certification).
+//  staging   interior tiles: the u8 tile + halo arrives by one TMA box
+//            (cp.async.bulk.tensor.3d + mbarrier); other tiles load rows
+//            directly with clamping.
+//  phase 1   each warp streams a quarter of the tile's 36 blurred rows: u8 ->
+//            fp32 by byte-permute + one FADD2, vertical blur from a register
+//            ring of the last 2R+1 rows (f32x2 FFMA2 on column pairs),
+//            horizontal blur with neighbour lanes' columns from 64-bit
+//            shuffles; the blurred rows land in shared memory (b tile).
+//  phase 2   (v3, default) the 4 warps split the tile's 34 magnitude rows once:
+//            Sobel from the b tile, squared magnitude into a shared m tile;
+//            4-pixel groups certainly below `low` are written as background
+//            right away, the others set a bit in their row's candidate word.
+//  phase 3   after one barrier each warp compacts the non-empty candidate
+//            words of its rows and classifies 32 groups at a time with every
+//            lane busy (sector, NMS, thresholds, certification); the fused
+//            pipeline's foreground bit planes are ORed in here.
+//  (v2, EF_K1_V2=1: per-warp magnitude rings and queues, kept for A/B runs.)
 //
 // Border policy (np.pad edge at every stage): input rows/columns clamped on
 // load; blurred and magnitude values at out-of-frame columns are replaced by
-// the edge column's value (warp shuffle); magnitude rows -1 and H alias rows
-// 0 and H-1 in the ring.
+// the edge column's value (warp shuffle); magnitude rows -1 and H copy rows 0
+// and H-1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -545,8 +549,8 @@ struct V3Smem {
         float m[V3_MROWS][V2_COLS];                 // squared magnitudes
         unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
     };
-    unsigned cmask[V2_TH];                          // candidate groups per output row (bit = lane)
-    unsigned short q[V2_WARPS][V3_QCAP];            // per-warp compaction queue: row << 8 | group
+    unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
+    unsigned short q[V2_WARPS][V3_QCAP];            // per-warp compaction queue: row << 7 | column
     unsigned long long mbar;
     FgBits bits;
 };
@@ -590,12 +594,16 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     float d[3][4], sm[3][4];
     sobel_row(brow(y0 - 2 + j0), d[0], sm[0]);
     sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
+    static_assert(V3_MPW % 3 == 0, "row ring period");
+#pragma unroll 1
+    for (int u3 = 0; u3 < V3_MPW; u3 += 3)
 #pragma unroll
-    for (int u = 0; u < V3_MPW; ++u) {
+    for (int u1 = 0; u1 < 3; ++u1) {
+        const int u = u3 + u1;
         const int j = j0 + u;
         if (j >= V3_MROWS) break;  // warp-uniform (last warp has 7 rows)
         const int Ym = y0 - 1 + j;
-        const int pu = u % 3, pm = (u + 1) % 3, pd = (u + 2) % 3;
+        const int pu = u1, pm = (u1 + 1) % 3, pd = (u1 + 2) % 3;
         sobel_row(brow(Ym + 1), d[pd], sm[pd]);
         const float2 two = f2(2.f, 2.f);
         const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[pd][0], d[pd][1])));
@@ -611,16 +619,14 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
             m23 = f2(m4[2], m4[3]);
         }
         *reinterpret_cast<float4*>(&S.m[j][l]) = make_float4(m01.x, m01.y, m23.x, m23.y);
-        // output rows: candidate bits, and the background class for the rest
+        // output rows: groups certainly below `low` get the background class
+        // now, the others are marked for the classifier
         if (j >= 1 && j <= V2_TH) {
-            const bool row_ok = INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH);
-            bool cand = false;
-            if (out_lane && row_ok) {
-                cand = fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
-                if (!cand) *lab = fill;
-            }
-            const unsigned ballot = __ballot_sync(0xffffffffu, cand);
-            if (lane == 0) S.cmask[j - 1] = ballot;
+            const bool act = out_lane && (INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH));
+            const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
+            if (act && !cand) *lab = fill;
+            const unsigned b0 = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) S.cmask[j - 1] = b0;
         }
         lab += Wq;
     }
@@ -630,30 +636,39 @@ template <int R>
 __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
                                          const V2Out O) {
     const int FH = P.FH;
+    // this warp's 8 candidate words (rows warp + 4 i), one per lane; only
+    // non-empty words are visited
+    const unsigned word = lane < V2_TH / V2_WARPS ? S.cmask[warp + V2_WARPS * lane] : 0u;
+    unsigned nz = __ballot_sync(0xffffffffu, word != 0u);
     int qn = 0;
-    // rows warp, warp + 4, ...: compact the candidate groups, classify 32 at a time
-    for (int r = warp; r < V2_TH; r += V2_WARPS) {
-        const unsigned mask = S.cmask[r];
-        if ((mask >> lane) & 1u) S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 8) | lane);
-        qn += __popc(mask);
-        const bool last = r + V2_WARPS >= V2_TH;
-        while (qn >= 32 || (last && qn > 0)) {
-            __syncwarp();
-            const int take = min(qn, 32);
-            if (lane < take) {
-                const int e = S.q[warp][lane];
-                const int Yc = y0 + (e >> 8), cl = e & 255, j = e >> 8;  // m tile row of Yc is j + 1
-                classify_group(P, xv0, Yc, cl, S.m[j], S.m[j + 1], S.m[j + 2],
-                               S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)], S.b[Yc - (y0 - 2)],
-                               S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)], S.bits, O);
-            }
-            __syncwarp();
-            const int rest = qn - take;
-            const unsigned short moved = lane < rest ? S.q[warp][32 + lane] : 0;
-            __syncwarp();
-            if (lane < rest) S.q[warp][lane] = moved;
-            qn = rest;
+    while (nz || qn) {
+        if (nz) {  // append one word's pixels
+            const int i = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const unsigned mask = __shfl_sync(0xffffffffu, word, i);
+            const int r = warp + V2_WARPS * i;
+            if ((mask >> lane) & 1u)
+                S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 7) | lane);
+            qn += __popc(mask);
+            if (qn < 32 && nz) continue;
         }
+        // classify 32 (or the last few) with every lane busy
+        __syncwarp();
+        const int take = min(qn, 32);
+        if (lane < take) {
+            const int e = S.q[warp][lane];
+            const int j = e >> 7, Yc = y0 + j;  // m tile row of Yc is j + 1
+            const float* bu = S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)];
+            const float* bd = S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)];
+            classify_group(P, xv0, Yc, e & 127, S.m[j], S.m[j + 1], S.m[j + 2], bu, S.b[Yc - (y0 - 2)], bd, S.bits,
+                           O);
+        }
+        __syncwarp();
+        const int rest = qn - take;
+        const unsigned short moved = lane < rest ? S.q[warp][32 + lane] : 0;
+        __syncwarp();
+        if (lane < rest) S.q[warp][lane] = moved;
+        qn = rest;
         __syncwarp();
     }
 }
@@ -674,13 +689,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (threadIdx.x == 0) S.bits = B;
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
-    if (interior) {
-        if (use_tma) {
-            tma_stage<R>(S, tmap, xv0, y0, g);
-            v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
-        } else {
-            v2_phase1<R, true, false>(img, g, xv0, y0, P, S, warp, lane);
-        }
+    // interior tiles take the TMA-staged fast path; without TMA (W % 16 != 0)
+    // every tile takes the general path -- one interior variant less keeps the
+    // kernel's hot code inside the instruction cache
+    if (interior && use_tma) {
+        tma_stage<R>(S, tmap, xv0, y0, g);
+        v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
         v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
         __syncthreads();
