@@ -318,6 +318,78 @@ __device__ __forceinline__ void classify_group(const V2Cls& P, int xv0, int Yc, 
     }
 }
 
+// Branch-free form of classify_group: the group's 6 columns (cc0-1 .. cc0+4) of
+// the three magnitude and three blurred rows are loaded once (one 16-byte and
+// two scalar loads per row), and every pixel's class, sector and NMS decision
+// is computed with selects -- lanes of a warp classify different groups, so
+// branches would serialise every path.
+__device__ __forceinline__ void load6(const float* row, int cc0, float (&v)[6]) {
+    const float4 mid = *reinterpret_cast<const float4*>(row + cc0);
+    v[0] = row[cc0 - 1];
+    v[1] = mid.x; v[2] = mid.y; v[3] = mid.z; v[4] = mid.w;
+    v[5] = row[cc0 + 4];
+}
+
+__device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
+                                                  const float* mc, const float* md, const float* bu,
+                                                  const float* bm, const float* bd, const FgBits& bits,
+                                                  const V2Out& O) {
+    const float t1 = 0.41421356237309503f;
+    const int cc0 = 4 * cl;
+    float Mu[6], Mc[6], Md[6], Bu[6], Bm[6], Bd[6];
+    load6(mu, cc0, Mu);
+    load6(mc, cc0, Mc);
+    load6(md, cc0, Md);
+    load6(bu, cc0, Bu);
+    load6(bm, cc0, Bm);
+    load6(bd, cc0, Bd);
+    uint32_t packed = 0;
+    bool any_flag = false;
+    const uint32_t cls0 = (uint32_t)P.cls0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float c = sqrt_apx(Mc[k + 1]);
+        const float gx = fmaf(2.f, Bm[k + 2] - Bm[k], (Bu[k + 2] - Bu[k]) + (Bd[k + 2] - Bd[k]));
+        const float gy = fmaf(2.f, Bd[k + 1], Bd[k] + Bd[k + 2]) - fmaf(2.f, Bu[k + 1], Bu[k] + Bu[k + 2]);
+        const float a = fabsf(gx), b = fabsf(gy);
+        const float uu = fmaf(t1, a, -b), vv = fmaf(t1, b, -a);
+        // neighbours along the sector: 0 (W/E), 90 (N/S), 45 (NE/SW), 135 (NW/SE)
+        const float n0 = fmaxf(Mc[k], Mc[k + 2]);
+        const float n90 = fmaxf(Mu[k + 1], Md[k + 1]);
+        const float n45 = fmaxf(Mu[k + 2], Md[k]);
+        const float n135 = fmaxf(Mu[k], Md[k + 2]);
+        const float ndiag = ((gx > 0.f) == (gy > 0.f)) ? n45 : n135;
+        const float nmax = uu > 0.f ? n0 : (vv > 0.f ? n90 : ndiag);
+        const float d = c - sqrt_apx(nmax);
+        const bool amb = fabsf(uu) <= P.e_sec || fabsf(vv) <= P.e_sec;
+        // threshold class: 2 / 1 / 0, or -1 inside a certification band
+        const int cls = c > P.hi_hi ? 2 : (c >= P.hi_lo ? -1 : (c > P.lo_hi ? 1 : (c >= P.lo_lo ? -1 : 0)));
+        const bool need_nms = cls >= 0 && (uint32_t)cls != cls0;
+        const bool flag = cls < 0 || (need_nms && (amb || fabsf(d) <= P.e_nms));
+        const uint32_t lab = flag ? (uint32_t)kFlag : ((need_nms && d > P.e_nms) ? (uint32_t)cls : cls0);
+        any_flag |= flag;
+        packed |= lab << (8 * k);
+    }
+    const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * P.W;
+    if (any_flag) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (((packed >> (8 * k)) & 0xffu) != kFlag) continue;
+            const unsigned long long slot = atomicAdd(&O.hdr->fix_count, 1ull);
+            if (slot < O.hdr->fix_cap) O.fix_list[slot] = rowbase + (unsigned long long)(xv0 + cc0 + k);
+            else O.hdr->overflow = 1u;
+        }
+    }
+    *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
+    if (bits.fg) {
+        // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
+        const uint32_t lo = packed & 0x03030303u;
+        const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;
+        const uint32_t stn = (((packed >> 1) & 0x01010101u) * 0x10204080u) >> 28;
+        if (fgn) fg_bits_or(bits, blockIdx.z, Yc - P.out0, xv0 + cc0, fgn, stn);
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0, int Yc, int cl, V2Smem& S,
                                                   int warp, const V2Out O) {
@@ -660,8 +732,8 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
             const int j = e >> 7, Yc = y0 + j;  // m tile row of Yc is j + 1
             const float* bu = S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)];
             const float* bd = S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)];
-            classify_group(P, xv0, Yc, e & 127, S.m[j], S.m[j + 1], S.m[j + 2], bu, S.b[Yc - (y0 - 2)], bd, S.bits,
-                           O);
+            classify_group_bf(P, xv0, Yc, e & 127, S.m[j], S.m[j + 1], S.m[j + 2], bu, S.b[Yc - (y0 - 2)], bd,
+                              S.bits, O);
         }
         __syncwarp();
         const int rest = qn - take;
