@@ -57,7 +57,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
-    size_t hdr, fix, perim, gpar, gstrong, pending, plist_idx, plist_node, plist_count, node_list, node_count,
+    size_t hdr, fix, perim, gpar, gstrong, pending, border, plist_idx, plist_node, plist_count, node_list, node_count,
         pend_tiles, dense, fgbits, stbits, plane_bytes, total;
     unsigned long long fix_cap, plist_scap, node_scap;
     HystLayout hl;
@@ -80,6 +80,8 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     L.gstrong = off;
     off = align_up(off + (size_t)L.hl.slots);
     L.pending = off;
+    off = align_up(off + (size_t)L.hl.tiles);
+    L.border = off;
     off = align_up(off + (size_t)L.hl.tiles);
     L.plist_scap = std::max<unsigned long long>(1ull << 10, npx / 64 / PL_STRIPES);
     L.plist_idx = off;
@@ -123,6 +125,7 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.gpar = reinterpret_cast<int*>(p + L.gpar);
     w.hb.gstrong = reinterpret_cast<uint8_t*>(p + L.gstrong);
     w.hb.pending = reinterpret_cast<uint8_t*>(p + L.pending);
+    w.hb.border = reinterpret_cast<uint8_t*>(p + L.border);
     w.hb.plist_idx = reinterpret_cast<unsigned long long*>(p + L.plist_idx);
     w.hb.plist_node = reinterpret_cast<int*>(p + L.plist_node);
     w.hb.plist_count = reinterpret_cast<unsigned long long*>(p + L.plist_count);

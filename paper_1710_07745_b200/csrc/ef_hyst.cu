@@ -411,6 +411,7 @@ __device__ __forceinline__ void hyst_block_tile(const uint8_t* __restrict__ labe
     if (row < g.vh && seg < g.vw)
         store32(final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg, g.vw - seg, fin);
     // perimeter slots p = tid and tid + 128: node id of the component at the slot
+    int any_node = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int p = tid + h * H_THREADS;
@@ -438,8 +439,11 @@ __device__ __forceinline__ void hyst_block_tile(const uint8_t* __restrict__ labe
             }
         }
         b.perim[tile * HP + p] = node;
+        any_node |= node >= 0;
     }
+    any_node = __syncthreads_or(any_node);
     if (tid == 0) {
+        b.border[tile] = any_node ? 1 : 0;
         b.pending[tile] = (uint8_t)s.pending;
         if (s.pending) atomicAdd(&b.pend_tiles[tile % PL_STRIPES], 1ull);
     }
@@ -743,7 +747,21 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
     }
     // ---- perimeter slots (lane handles slots lane + 32 j): node id of the
-    // component at each slot; a component's own (smallest) slot makes it a node
+    // component at each slot; a component's own (smallest) slot makes it a node.
+    // A tile without foreground on its perimeter writes nothing here: its
+    // border flag tells every reader of perim[] (H2, H3's fallback scan, the
+    // band-edge export) to skip it.
+    const unsigned long long vmask = g.vw == HT ? ~0ull : ((1ull << g.vw) - 1ull);
+    const bool per_fg = __any_sync(0xffffffffu, ((f0 | f1) & (1ull | (1ull << (g.vw - 1)))) != 0ull) ||
+                        ((s.fgrow[0] | s.fgrow[g.vh - 1]) & vmask) != 0ull;
+    if (!per_fg) {
+        if (lane == 0) {
+            b.border[tile] = 0;
+            b.pending[tile] = (uint8_t)tile_pending;
+            if (tile_pending) atomicAdd(&b.pend_tiles[stripe], 1ull);
+        }
+        return;
+    }
     int nodes[HP / 32];
     unsigned own[HP / 32];
     int total = 0;
@@ -795,58 +813,67 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
     }
     if (lane == 0) {
+        b.border[tile] = 1;
         b.pending[tile] = (uint8_t)tile_pending;
         if (tile_pending) atomicAdd(&b.pend_tiles[stripe], 1ull);
     }
 }
 
-// H2: unions across tile seams.  128 threads per tile: 0..63 right seam rows,
-// 64..127 bottom seam columns; thread 0 also does the two corner diagonals.
-__global__ void __launch_bounds__(128)
-hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, const int* __restrict__ perim, int* gpar) {
-    const long long tile = tile_id_xyz(tiles_x, tiles_y);
-    TileGeo g = tile_geo_xyz(blockIdx.x, blockIdx.y, blockIdx.z, H, W);
-    const int t = threadIdx.x;
-    const int* pa = perim + tile * HP;
-    if (t < 64) {
-        if (g.txi + 1 < tiles_x && t < g.vh) {
-            int a = pa[192 + t];
-            if (a >= 0) {
-                const int* pb = perim + (tile + 1) * HP;
-                for (int dy = -1; dy <= 1; ++dy) {
-                    int y2 = t + dy;
-                    if (y2 < 0 || y2 >= g.vh) continue;
-                    int b = pb[128 + y2];
-                    if (b >= 0) gunite(gpar, a, b);
-                }
+// H2: unions across tile seams, one warp per tile (8 per block; grid
+// (ceil(tiles per frame / 8), frames)): right seam rows, bottom seam columns,
+// and the two lower corner diagonals.  Tiles without perimeter components --
+// and seams whose other side has none -- are skipped on one byte.
+__global__ void __launch_bounds__(256)
+hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tpf = tiles_x * tiles_y;
+    const int t = blockIdx.x * 8 + warp;
+    if (t >= tpf) return;
+    const long long tile = (long long)blockIdx.y * tpf + t;
+    if (!b.border[tile]) return;
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    const TileGeo g = tile_geo_xyz(tx, ty, blockIdx.y, H, W);
+    const int* pa = b.perim + tile * HP;
+    int* gpar = b.gpar;
+    if (tx + 1 < tiles_x && b.border[tile + 1]) {
+        const int* pb = b.perim + (tile + 1) * HP;
+        for (int r = lane; r < g.vh; r += 32) {
+            const int a = pa[192 + r];
+            if (a < 0) continue;
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int y2 = r + dy;
+                if (y2 < 0 || y2 >= g.vh) continue;
+                const int c = pb[128 + y2];
+                if (c >= 0) gunite(gpar, a, c);
             }
         }
-    } else {
-        int x = t - 64;
-        if (g.tyi + 1 < tiles_y && x < g.vw) {
-            int a = pa[64 + x];
-            if (a >= 0) {
-                const int* pc = perim + (tile + tiles_x) * HP;
-                TileGeo gc = tile_geo_xyz(blockIdx.x, blockIdx.y + 1, blockIdx.z, H, W);
+    }
+    if (ty + 1 < tiles_y) {
+        const TileGeo gc = tile_geo_xyz(tx, ty + 1, blockIdx.y, H, W);
+        if (b.border[tile + tiles_x]) {
+            const int* pc = b.perim + (tile + tiles_x) * HP;
+            for (int x = lane; x < g.vw; x += 32) {
+                const int a = pa[64 + x];
+                if (a < 0) continue;
                 for (int dx = -1; dx <= 1; ++dx) {
-                    int x2 = x + dx;
+                    const int x2 = x + dx;
                     if (x2 < 0 || x2 >= gc.vw) continue;
-                    int c = pc[x2];
+                    const int c = pc[x2];
                     if (c >= 0) gunite(gpar, a, c);
                 }
             }
         }
-    }
-    if (t == 0 && g.tyi + 1 < tiles_y) {
-        if (g.txi + 1 < tiles_x && g.vw == HT) {  // bottom-right corner -> tile below-right (0,0)
-            int a = pa[64 + HT - 1];
-            int d = perim[(tile + tiles_x + 1) * HP + 0];
-            if (a >= 0 && d >= 0) gunite(gpar, a, d);
-        }
-        if (g.txi > 0) {  // bottom-left corner -> tile below-left (0, 63)
-            int a = pa[64 + 0];
-            int d = perim[(tile + tiles_x - 1) * HP + HT - 1];
-            if (a >= 0 && d >= 0) gunite(gpar, a, d);
+        if (lane == 0) {
+            if (tx + 1 < tiles_x && g.vw == HT && b.border[tile + tiles_x + 1]) {  // bottom-right -> (0,0) below-right
+                const int a = pa[64 + HT - 1];
+                const int d = b.perim[(tile + tiles_x + 1) * HP + 0];
+                if (a >= 0 && d >= 0) gunite(gpar, a, d);
+            }
+            if (tx > 0 && b.border[tile + tiles_x - 1]) {  // bottom-left -> (0, 63) below-left
+                const int a = pa[64 + 0];
+                const int d = b.perim[(tile + tiles_x - 1) * HP + HT - 1];
+                if (a >= 0 && d >= 0) gunite(gpar, a, d);
+            }
         }
     }
 }
@@ -860,6 +887,7 @@ __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr)
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         int node;
         if (all) {
+            if (!b.border[e / HP]) continue;  // perim[] of a tile without border components is stale
             node = b.perim[e];
             if (node != (int)e) continue;  // the node's own (smallest) slot only
         } else {
@@ -947,15 +975,15 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
 // Band edge export: component root id and strong flag for the top and bottom
 // rows of a band (the frame of `rows` rows).
 __global__ void band_edges_kernel(int rows, int W, int tiles_x, int tiles_y, const int* __restrict__ perim,
-                                  const int* __restrict__ gpar, const uint8_t* __restrict__ gstrong,
-                                  int64_t* ids, uint8_t* strong) {
+                                  const uint8_t* __restrict__ border, const int* __restrict__ gpar,
+                                  const uint8_t* __restrict__ gstrong, int64_t* ids, uint8_t* strong) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2 * W) return;
     bool bottom = t >= W;
     int x = bottom ? t - W : t;
     long long tile = (long long)(bottom ? tiles_y - 1 : 0) * tiles_x + x / HT;
     int slot = (bottom ? 64 : 0) + x % HT;
-    int node = perim[tile * HP + slot];
+    int node = border[tile] ? perim[tile * HP + slot] : -1;
     if (node < 0) { ids[t] = -1; strong[t] = 0; return; }
     int r = gfind_ro(gpar, node);
     ids[t] = r;
@@ -963,13 +991,14 @@ __global__ void band_edges_kernel(int rows, int W, int tiles_x, int tiles_y, con
 }
 
 __global__ void band_apply_kernel(int rows, int W, int tiles_x, int tiles_y, const int* __restrict__ perim,
-                                  const int* __restrict__ gpar, uint8_t* gstrong,
-                                  const uint8_t* __restrict__ strong_edges) {
+                                  const uint8_t* __restrict__ border, const int* __restrict__ gpar,
+                                  uint8_t* gstrong, const uint8_t* __restrict__ strong_edges) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2 * W || !strong_edges[t]) return;
     bool bottom = t >= W;
     int x = bottom ? t - W : t;
     long long tile = (long long)(bottom ? tiles_y - 1 : 0) * tiles_x + x / HT;
+    if (!border[tile]) return;
     int node = perim[tile * HP + (bottom ? 64 : 0) + x % HT];
     if (node >= 0) gstrong[gfind_ro(gpar, node)] = 1;
 }
@@ -988,7 +1017,6 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                               const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
                               cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    const dim3 tgrid(L.tiles_x, L.tiles_y, (unsigned)batch);
     cudaFuncSetAttribute(hyst_local_warp_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1008,7 +1036,8 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
     hyst_dense_kernel<<<sm_count * 4, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    hyst_merge_kernel<<<tgrid, 128, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b.perim, b.gpar);
+    const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);
+    hyst_merge_kernel<<<mgrid, 256, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long blocks = (L.slots + 255) / 256;
@@ -1031,7 +1060,7 @@ cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W
 cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
                               cudaStream_t st) {
     HystLayout L = hyst_layout(1, rows, W);
-    band_edges_kernel<<<(2 * W + 255) / 256, 256, 0, st>>>(rows, W, L.tiles_x, L.tiles_y, b.perim, b.gpar,
+    band_edges_kernel<<<(2 * W + 255) / 256, 256, 0, st>>>(rows, W, L.tiles_x, L.tiles_y, b.perim, b.border, b.gpar,
                                                            b.gstrong, ids, strong);
     return cudaGetLastError();
 }
@@ -1039,7 +1068,7 @@ cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, 
 cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,
                               cudaStream_t st) {
     HystLayout L = hyst_layout(1, rows, W);
-    band_apply_kernel<<<(2 * W + 255) / 256, 256, 0, st>>>(rows, W, L.tiles_x, L.tiles_y, b.perim, b.gpar,
+    band_apply_kernel<<<(2 * W + 255) / 256, 256, 0, st>>>(rows, W, L.tiles_x, L.tiles_y, b.perim, b.border, b.gpar,
                                                            b.gstrong, strong_edges);
     return cudaGetLastError();
 }

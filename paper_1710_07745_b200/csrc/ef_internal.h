@@ -32,6 +32,7 @@ struct HystBufs {
     int* gpar;
     uint8_t* gstrong;
     uint8_t* pending;
+    uint8_t* border;  // per tile: some perimeter slot holds a component (H1 -> H2)
     unsigned long long* plist_idx;  // pixels of undecided border components (H1 -> H4),
     int* plist_node;                //   PL_STRIPES stripes of plist_scap entries
     unsigned long long* plist_count;  // per stripe
