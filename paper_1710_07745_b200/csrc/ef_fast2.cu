@@ -650,7 +650,11 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     constexpr int HXA = V2Cfg<R>::HXA;
     constexpr int OW = V2Cfg<R>::OW;
     const int W = g.W, FH = g.full_H;
-    const int j0 = warp * V3_MPW;  // this warp's magnitude rows j0 .. j0+8 (tile rows; Ym = y0 - 1 + j)
+    // this warp's magnitude rows j0 .. j0+8 (tile rows; Ym = y0 - 1 + j).  The
+    // last warp starts at 25 so every warp runs exactly 9 rows (no divergent
+    // loop exit around the shuffles and votes); rows 25 and 26 are computed
+    // twice, with identical values, labels and candidate words.
+    const int j0 = min(warp * V3_MPW, V3_MROWS - V3_MPW);
     const int oy0 = g.out0, oy1 = g.out0 + g.rows;
     const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
     const int c = xv0 + 4 * lane;
@@ -673,7 +677,6 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     for (int u1 = 0; u1 < 3; ++u1) {
         const int u = u3 + u1;
         const int j = j0 + u;
-        if (j >= V3_MROWS) break;  // warp-uniform (last warp has 7 rows)
         const int Ym = y0 - 1 + j;
         const int pu = u1, pm = (u1 + 1) % 3, pd = (u1 + 2) % 3;
         sobel_row(brow(Ym + 1), d[pd], sm[pd]);
