@@ -255,8 +255,7 @@ bool has_negative(const double* w, int r) {
 }
 
 // fin != nullptr (fused pipeline): where the production classifier runs, it
-// also fills the workspace's foreground bit planes, fin is zeroed for the
-// hysteresis to write only final pixels, and *bits describes the planes
+// also fills the workspace's foreground bit planes and *bits describes them
 // (bits->fg == nullptr otherwise).
 int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const double* w, int r,
                     double low, double high, uint8_t* labels, const Ws& ws, const WsLayout& L,
@@ -284,7 +283,7 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
         const size_t plane = (size_t)batch * g.rows * words * sizeof(unsigned long long);
         EF_CHECK(cudaMemsetAsync(ws.fgbits, 0, plane, st), "bit planes");
         EF_CHECK(cudaMemsetAsync(ws.stbits, 0, plane, st), "bit planes");
-        EF_CHECK(cudaMemsetAsync(fin, 0, (size_t)batch * g.rows * g.W, st), "final");
+
         *bits = B;
     }
     const Timing& T = timing();

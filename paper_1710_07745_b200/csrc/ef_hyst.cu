@@ -542,9 +542,8 @@ __device__ __forceinline__ int row_of(const WarpTile& s, int e) {
 }
 
 // BITS: the fused pipeline -- the classifier ORed the foreground / strong
-// pixels into bit planes and final_out was zeroed, so a tile reads 2 bits per
-// pixel (no label bytes) and stores one byte per final pixel.  Otherwise the
-// label bytes are read and the whole final tile is written.
+// pixels into bit planes, so a tile reads 2 bits per pixel instead of its
+// label bytes.  Either way the whole final tile is written.
 // Grid: (ceil(tiles per frame / WT_WARPS), frames); one warp per tile.
 template <bool BITS>
 __global__ void __launch_bounds__(32 * WT_WARPS)
@@ -646,15 +645,6 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         s.finrow[2 * lane + 1] = 0ull;
         __syncwarp();
     }
-    auto store_final = [&](int r, int x) {
-        final_out[frame_off + (size_t)(g.y0 + r) * W + g.x0 + x] = 1;
-    };
-    if (kind == 1 && BITS) {
-        for (int e = lane; e < n; e += 32) {
-            const int r = row_of(s, e);
-            store_final(r, select64(s.fgrow[r], e - s.rowbase[r]));
-        }
-    }
     if (kind == 2) {
         // compact list + union-find init, lane-balanced: index e -> (row, column)
         // by the prefix counts; runs are pre-linked to their start
@@ -705,8 +695,7 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
                 pix = s.list[e];
                 v = s.info[s.par[e]];
                 if (info_strong(v)) {
-                    if (BITS) store_final(pix >> 6, pix & (HT - 1));
-                    else atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
+                    atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
                 } else {
                     pend = info_slot(v) != NO_SLOT;
                 }
@@ -729,8 +718,9 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
         __syncwarp();
     }
-    if (!BITS) {
-        // ---- whole final tile (4 lanes per row, 16 bytes each)
+    {
+        // ---- whole final tile (4 lanes per row, 16 bytes each): one pass
+        // writes the zeros too (cheaper than a memset of final before K1)
         const bool full_out = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(final_out) & 15) == 0);
 #pragma unroll 2
         for (int it = 0; it < HT / 8; ++it) {
