@@ -14,7 +14,7 @@
 //            ring of the last 2R+1 rows (f32x2 FFMA2 on column pairs),
 //            horizontal blur with neighbour lanes' columns from 64-bit
 //            shuffles; the blurred rows land in shared memory (b tile).
-//  phase 2   (v3, default) the 4 warps split the tile's 34 magnitude rows once:
+//  phase 2   the 4 warps split the tile's 34 magnitude rows once:
 //            Sobel from the b tile, squared magnitude into a shared m tile;
 //            4-pixel groups certainly below `low` are written as background
 //            right away, the others set a bit in their row's candidate word.
@@ -22,7 +22,8 @@
 //            words of its rows and classifies 32 groups at a time with every
 //            lane busy (sector, NMS, thresholds, certification); the fused
 //            pipeline's foreground bit planes are ORed in here.
-//  (v2, EF_K1_V2=1: per-warp magnitude rings and queues, kept for A/B runs.)
+//  (v2 -- per-warp magnitude rings recomputing 4 halo rows per 8, queues
+//  flushed on a timer, branchy classifier -- needed 20% more instructions.)
 //
 // Border policy (np.pad edge at every stage): input rows/columns clamped on
 // load; blurred and magnitude values at out-of-frame columns are replaced by
@@ -44,9 +45,6 @@ constexpr int V2_THREADS = 32 * V2_WARPS;
 constexpr int V2_COLS = 128;
 constexpr int V2_TH = 32;
 constexpr int V2_BROWS = V2_TH + 4;
-constexpr int V2_ROWS_PER_WARP = V2_TH / V2_WARPS;
-constexpr int MRING = 8;
-constexpr int QCAP = 128;
 
 constexpr int V2_MAXR = 6;
 constexpr int V2_IN_ROWS = V2_BROWS + 2 * V2_MAXR;  // staged u8 input rows (TMA box height <= this)
@@ -60,17 +58,6 @@ struct V2Out {
     unsigned long long out_base;
     unsigned long long* fix_list;
     WsHeader* hdr;
-};
-
-struct V2Smem {
-    float b[V2_BROWS][V2_COLS];
-    union {
-        float m[V2_WARPS][MRING][V2_COLS];            // phase 2: magnitude rings
-        unsigned char in[V2_IN_ROWS][V2_IN_COLS];     // phase 1: TMA-staged input tile + halo
-    };
-    int q[V2_WARPS][QCAP];
-    unsigned long long mbar;                           // TMA completion barrier
-    FgBits bits;  // the classifier's bit planes (bits.fg == nullptr: off); read by the out-of-line classifier
 };
 
 template <int R>
@@ -250,75 +237,9 @@ struct V2Cls {
 };
 
 
-__device__ __forceinline__ int mslot(int Y) { return (Y + MRING) & (MRING - 1); }
 
-// Classify the 4 pixels of one candidate group (certified; kFlag otherwise):
-// mu/mc/md are the squared-magnitude rows Yc-1, Yc, Yc+1 and bu/bm/bd the
-// blurred rows (clamped) of the tile, indexed by tile column.
-__device__ __forceinline__ void classify_group(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
-                                               const float* mc, const float* md, const float* bu, const float* bm,
-                                               const float* bd, const FgBits& bits, const V2Out& O) {
-    const int W = P.W;
-    const float t1 = 0.41421356237309503f;
-    uint32_t packed = 0;
-    const int cc0 = 4 * cl;
-    const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * W;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int cc = cc0 + k;
-        const float c = sqrt_apx(mc[cc]);
-        int cls;
-        if (c > P.hi_hi) cls = 2;
-        else if (c >= P.hi_lo) cls = -1;
-        else if (c > P.lo_hi) cls = 1;
-        else if (c >= P.lo_lo) cls = -1;
-        else cls = 0;
-        bool flag = cls < 0;
-        uint32_t lab = (uint32_t)P.cls0;
-        if (!flag && cls != P.cls0) {
-            float dxu = bu[cc + 1] - bu[cc - 1];
-            float dxm = bm[cc + 1] - bm[cc - 1];
-            float dxd = bd[cc + 1] - bd[cc - 1];
-            float su = fmaf(2.f, bu[cc], bu[cc - 1] + bu[cc + 1]);
-            float sd = fmaf(2.f, bd[cc], bd[cc - 1] + bd[cc + 1]);
-            float gx = fmaf(2.f, dxm, dxu + dxd);
-            float gy = sd - su;
-            float a = fabsf(gx), b = fabsf(gy);
-            float uu = fmaf(t1, a, -b), vv = fmaf(t1, b, -a);
-            if (fabsf(uu) <= P.e_sec || fabsf(vv) <= P.e_sec) {
-                flag = true;
-            } else {
-                float n1, n2;  // squared magnitudes of the two neighbours along the sector
-                if (uu > 0.f) { n1 = mc[cc - 1]; n2 = mc[cc + 1]; }                       // 0
-                else if (vv > 0.f) { n1 = mu[cc]; n2 = md[cc]; }                          // 90
-                else if ((gx > 0.f) == (gy > 0.f)) { n1 = mu[cc + 1]; n2 = md[cc - 1]; }  // 45
-                else { n1 = mu[cc - 1]; n2 = md[cc + 1]; }                                // 135
-                float d = c - sqrt_apx(fmaxf(n1, n2));
-                if (d < -P.e_nms) lab = (uint32_t)P.cls0;
-                else if (d > P.e_nms) lab = (uint32_t)cls;
-                else flag = true;
-            }
-        }
-        if (flag) {
-            lab = kFlag;
-            const unsigned long long o = rowbase + (unsigned long long)(xv0 + cc);
-            unsigned long long slot = atomicAdd(&O.hdr->fix_count, 1ull);
-            if (slot < O.hdr->fix_cap) O.fix_list[slot] = o;
-            else O.hdr->overflow = 1u;
-        }
-        packed |= lab << (8 * k);
-    }
-    *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
-    if (bits.fg) {
-        // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
-        const uint32_t lo = packed & 0x03030303u;
-        const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;
-        const uint32_t stn = (((packed >> 1) & 0x01010101u) * 0x10204080u) >> 28;
-        if (fgn) fg_bits_or(bits, blockIdx.z, Yc - P.out0, xv0 + cc0, fgn, stn);
-    }
-}
-
-// Branch-free form of classify_group: the group's 6 columns (cc0-1 .. cc0+4) of
+// Classify the 4 pixels of one candidate group (certified; kFlag otherwise),
+// branch-free: the group's 6 columns (cc0-1 .. cc0+4) of
 // the three magnitude and three blurred rows are loaded once (one 16-byte and
 // two scalar loads per row), and every pixel's class, sector and NMS decision
 // is computed with selects -- lanes of a warp classify different groups, so
@@ -390,151 +311,6 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
     }
 }
 
-template <int R>
-__device__ __forceinline__ void v2_classify_group(const V2Cls P, int xv0, int y0, int Yc, int cl, V2Smem& S,
-                                                  int warp, const V2Out O) {
-    const int FH = P.FH;
-    classify_group(P, xv0, Yc, cl, S.m[warp][mslot(Yc - 1)], S.m[warp][mslot(Yc)], S.m[warp][mslot(Yc + 1)],
-                   S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)], S.b[Yc - (y0 - 2)],
-                   S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)], S.bits, O);
-}
-
-template <int R>
-__device__ __noinline__ int v2_flush(const V2Cls P, int xv0, int y0, int qn, V2Smem& S, int warp, int lane,
-                                     const V2Out O) {
-    // every queued group is classified; at most QCAP - 32 stay behind
-    while (qn > 0) {
-        const int take = min(qn, 32);
-        if (lane < take) {
-            const int e = S.q[warp][lane];
-            v2_classify_group<R>(P, xv0, y0, y0 + (e >> 8), e & 255, S, warp, O);
-        }
-        const int rest = qn - take;
-        int moved[QCAP / 32 - 1];
-#pragma unroll
-        for (int j = 0; j < QCAP / 32 - 1; ++j) moved[j] = (lane + 32 * j < rest) ? S.q[warp][32 + lane + 32 * j] : 0;
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < QCAP / 32 - 1; ++j)
-            if (lane + 32 * j < rest) S.q[warp][lane + 32 * j] = moved[j];
-        __syncwarp();
-        qn = rest;
-    }
-    return qn;
-}
-
-template <int R, bool INTERIOR>
-__device__ __forceinline__ void v2_phase2(const FrameGeom& g, int xv0, int y0, const FastParams& P, V2Smem& S,
-                                          int warp, int lane, const V2Out& O) {
-    constexpr int HXA = V2Cfg<R>::HXA;
-    constexpr int OW = V2Cfg<R>::OW;
-    constexpr int NSTEP = V2_ROWS_PER_WARP + 4;  // b rows Y0w-2 .. Y0w+17 (one extra no-op step)
-    const int W = g.W, FH = g.full_H;
-    const int Y0w = y0 + warp * V2_ROWS_PER_WARP;
-    const int oy0 = max(Y0w, g.out0), oy1 = min(Y0w + V2_ROWS_PER_WARP, g.out0 + g.rows);
-    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
-    const bool vclamp = !INTERIOR && (Y0w - 2 < 0 || Y0w + V2_ROWS_PER_WARP + 1 >= FH);
-    const int c = xv0 + 4 * lane;
-    // output lane: its 4 columns lie inside [x0, x0 + OW) and inside the frame
-    const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
-    const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
-    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, W, FH, g.out0};
-    const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
-    uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(Y0w - g.out0) * W + c);
-
-    const int Wq = W >> 2;
-    const int l = 4 * lane;
-    const float* bp = &S.b[Y0w - 2 - (y0 - 2)][l];
-    float* mring = S.m[warp][0];
-    int mslot_next = mslot(Y0w - 3);  // ring slot of row Ym at step t: mslot(Y0w - 3 + t)
-
-    float d[3][4], sm[3][4];
-    float2 mq[3][2];
-    int qn = 0, qprev = 0;
-    constexpr int NGRP = (NSTEP + 2) / 3;  // 7 groups of 3 steps; the 21st step is a no-op row
-#pragma unroll 1
-    for (int grp = 0; grp < NGRP; ++grp) {
-#pragma unroll
-        for (int ph = 0; ph < 3; ++ph) {
-            const int t = grp * 3 + ph;
-            const int jb = Y0w - 2 + t;
-            const float* brow = vclamp ? &S.b[clampi(jb, 0, FH - 1) - (y0 - 2)][l] : bp;
-            bp += V2_COLS;
-            const float4 bb = *reinterpret_cast<const float4*>(brow);
-            // neighbour lanes' edge columns (lane 0 / 31 get wrapped values: only
-            // columns no output depends on are affected)
-            const float bl = __shfl_up_sync(0xffffffffu, bb.w, 1);
-            const float br = __shfl_down_sync(0xffffffffu, bb.x, 1);
-            d[ph][0] = bb.y - bl;
-            d[ph][1] = bb.z - bb.x;
-            d[ph][2] = bb.w - bb.y;
-            d[ph][3] = br - bb.z;
-            sm[ph][0] = fmaf(2.f, bb.x, bl + bb.y);
-            sm[ph][1] = fmaf(2.f, bb.y, bb.x + bb.z);
-            sm[ph][2] = fmaf(2.f, bb.z, bb.y + bb.w);
-            sm[ph][3] = fmaf(2.f, bb.w, bb.z + br);
-            // squared magnitude of row Ym = jb-1 from b rows jb-2 (pu), jb-1 (pm), jb (ph)
-            // (meaningful from t >= 2; earlier steps store into ring rows no
-            // classification reads before they are rewritten)
-            const int pu = (ph + 1) % 3, pm = (ph + 2) % 3;
-            const float2 two = f2(2.f, 2.f);
-            const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[ph][0], d[ph][1])));
-            const float2 gx23 = fma2(two, f2(d[pm][2], d[pm][3]), add2(f2(d[pu][2], d[pu][3]), f2(d[ph][2], d[ph][3])));
-            const float2 gy01 = add2(f2(sm[ph][0], sm[ph][1]), f2(-sm[pu][0], -sm[pu][1]));
-            const float2 gy23 = add2(f2(sm[ph][2], sm[ph][3]), f2(-sm[pu][2], -sm[pu][3]));
-            float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
-            float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
-            if (edge) {
-                float m4[4] = {m01.x, m01.y, m23.x, m23.y};
-                edge_fix(m4, xv0, lane, W);
-                m01 = f2(m4[0], m4[1]);
-                m23 = f2(m4[2], m4[3]);
-            }
-            mq[ph][0] = m01;
-            mq[ph][1] = m23;
-            const int Ym = jb - 1;
-            float* mdst = mring + mslot_next * V2_COLS + l;
-            mslot_next = (mslot_next + 1) & (MRING - 1);
-            if (t >= 2) {
-                if (!vclamp || (Ym >= 0 && Ym < FH)) {
-                    *reinterpret_cast<float2*>(mdst) = m01;
-                    *reinterpret_cast<float2*>(mdst + 2) = m23;
-                }
-                if (vclamp && Ym == 0) {
-                    *reinterpret_cast<float2*>(mring + mslot(-1) * V2_COLS + l) = m01;
-                    *reinterpret_cast<float2*>(mring + mslot(-1) * V2_COLS + l + 2) = m23;
-                }
-                if (vclamp && Ym == FH - 1) {
-                    *reinterpret_cast<float2*>(mring + mslot(FH) * V2_COLS + l) = m01;
-                    *reinterpret_cast<float2*>(mring + mslot(FH) * V2_COLS + l + 2) = m23;
-                }
-            }
-            // row Yc = jb - 2: its squared magnitudes were produced one step ago
-            const int Yc = jb - 2;
-            const int pp = (ph + 2) % 3;
-            const bool row_ok = t >= 4 && (INTERIOR ? t < NSTEP : (Yc >= oy0 && Yc < oy1));
-            bool cand = false;
-            if (out_lane && row_ok) {
-                cand = fmaxf(fmaxf(mq[pp][0].x, mq[pp][0].y), fmaxf(mq[pp][1].x, mq[pp][1].y)) >= cand_sq;
-                if (!cand) *lab = fill;
-            }
-            if (t >= 4) lab += Wq;
-            const unsigned ballot = __ballot_sync(0xffffffffu, cand);
-            if (cand) S.q[warp][qn + __popc(ballot & ((1u << lane) - 1u))] = ((Yc - y0) << 8) | lane;
-            qn += __popc(ballot);
-        }
-        // classify queued groups when 32 are waiting, when entries have already
-        // waited one 3-step group (an entry for row Yc needs ring rows Yc-1..Yc+1;
-        // the 8-row ring reuses the slot of Yc-1 at step jb = Yc+8, and two groups
-        // after its enqueue step jb = Yc+2 is at most jb = Yc+7), or at the end
-        if (qn >= 32 || qprev > 0 || grp == NGRP - 1) {
-            __syncwarp();
-            qn = v2_flush<R>(CP, xv0, y0, qn, S, warp, lane, O);
-        }
-        qprev = qn;
-    }
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -566,40 +342,6 @@ __device__ __forceinline__ void tma_stage(Smem& S, const CUtensorMap& tmap, int 
             : "=r"(done)
             : "r"(bar)
             : "memory");
-    }
-}
-
-template <int R>
-__global__ void __launch_bounds__(V2_THREADS, 6)
-k1v2_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
-            unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
-            const __grid_constant__ CUtensorMap tmap, int use_tma, FgBits B) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V2Smem& S = *reinterpret_cast<V2Smem*>(smraw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x0 = blockIdx.x * V2Cfg<R>::OW;
-    const int xv0 = x0 - V2Cfg<R>::HXA;
-    const int y0 = g.out0 + blockIdx.y * V2_TH;
-    const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
-    V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
-    if (threadIdx.x == 0) S.bits = B;
-    // interior tile: every column and row of the halo exists in the buffer and
-    // every output row is classified -- no clamps, no predicated stores
-    const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
-                          y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
-    if (interior && use_tma) {
-        tma_stage<R>(S, tmap, xv0, y0, g);
-        v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
-        __syncthreads();
-        v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
-    } else if (interior) {
-        v2_phase1<R, true, false>(img, g, xv0, y0, P, S, warp, lane);
-        __syncthreads();
-        v2_phase2<R, true>(g, xv0, y0, P, S, warp, lane, O);
-    } else {
-        v2_phase1<R, false, false>(img, g, xv0, y0, P, S, warp, lane);
-        __syncthreads();
-        v2_phase2<R, false>(g, xv0, y0, P, S, warp, lane, O);
     }
 }
 
@@ -828,9 +570,8 @@ template <int R>
 static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                             uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
                             cudaStream_t st) {
-    static const bool v2 = getenv("EF_K1_V2") != nullptr;  // previous layout, for A/B runs
-    auto kern = v2 ? k1v2_kernel<R> : k1v3_kernel<R>;
-    const int smem = v2 ? (int)sizeof(V2Smem) : (int)sizeof(V3Smem);
+    auto kern = k1v3_kernel<R>;
+    const int smem = (int)sizeof(V3Smem);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     // occupancy is shared-memory bound: ask for the largest carveout
