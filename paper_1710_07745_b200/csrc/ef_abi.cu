@@ -496,14 +496,23 @@ int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double*
 //  * the packed staging lines are flushed from the CPU caches after the unpack:
 //    DMA writes into CPU-cached pinned lines ran ~3x slower and dragged the
 //    concurrent H2D down with them;
-//  * chunks ramp 2 -> 16 MB and back down, so the pipeline fills and drains
+//  * chunks ramp 1 -> 8 MB and back down, so the pipeline fills and drains
 //    quickly while the middle chunks are large enough for the kernels to keep
 //    up with the copy engine.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr int kHostStreams = 3;
 constexpr int kPackSlots = 2 * kHostStreams;  // packed chunks in flight (D2H or unpack)
-constexpr int kOverlapUnpackThreads = 4;
+// tunables (env overrides for measurement runs: EF_HOST_UNPACK_THREADS, EF_HOST_CHUNK_MB)
+int overlap_unpack_threads() {
+    static const int n = getenv("EF_HOST_UNPACK_THREADS") ? std::max(1, atoi(getenv("EF_HOST_UNPACK_THREADS"))) : 4;
+    return n;
+}
+size_t max_chunk_bytes() {
+    static const size_t n = getenv("EF_HOST_CHUNK_MB") ? std::max<size_t>(1, atoi(getenv("EF_HOST_CHUNK_MB"))) << 20
+                                                       : (size_t)8 << 20;
+    return n;
+}
 
 struct PackSlot {
     uint8_t* packed = nullptr;   // pinned
@@ -555,7 +564,7 @@ void wait_and_unpack(PackSlot* s, int device) {
         return;
     }
     HostPool& P = host_pool();
-    const size_t threads = s->last ? (size_t)P.size() : (size_t)std::min(P.size(), kOverlapUnpackThreads);
+    const size_t threads = s->last ? (size_t)P.size() : (size_t)std::min(P.size(), overlap_unpack_threads());
     const size_t parts = std::max<size_t>(1, std::min<size_t>(threads, s->nbytes / 16384));
     const size_t per = ((s->nbytes + parts - 1) / parts + 63) & ~size_t(63);
     const int n = (int)((s->nbytes + per - 1) / per);
@@ -605,8 +614,8 @@ bool drain(HostCtx& C) {
 
 // frames per chunk: ramp up from ~2 MB to ~16 MB, hold, ramp back down
 std::vector<int64_t> chunk_plan(int64_t batch, size_t fpx) {
-    const int64_t cmax = std::max<int64_t>(1, (int64_t)((16u << 20) / fpx));
-    const int64_t c0 = std::max<int64_t>(1, std::min<int64_t>(cmax, (int64_t)((2u << 20) / fpx)));
+    const int64_t cmax = std::max<int64_t>(1, (int64_t)(max_chunk_bytes() / fpx));
+    const int64_t c0 = std::max<int64_t>(1, std::min<int64_t>(cmax, (int64_t)((max_chunk_bytes() / 8) / fpx)));
     std::vector<int64_t> ramp;
     for (int64_t c = c0; c < cmax; c *= 2) ramp.push_back(c);
     int64_t ramp_sum = 0;
