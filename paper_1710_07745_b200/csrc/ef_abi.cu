@@ -612,7 +612,7 @@ bool drain(HostCtx& C) {
     return failed;
 }
 
-// frames per chunk: ramp up from ~2 MB to ~16 MB, hold, ramp back down
+// frames per chunk: ramp up from max/8 to the max chunk (8 MB), hold, ramp back down
 std::vector<int64_t> chunk_plan(int64_t batch, size_t fpx) {
     const int64_t cmax = std::max<int64_t>(1, (int64_t)(max_chunk_bytes() / fpx));
     const int64_t c0 = std::max<int64_t>(1, std::min<int64_t>(cmax, (int64_t)((max_chunk_bytes() / 8) / fpx)));
