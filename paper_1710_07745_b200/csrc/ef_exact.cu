@@ -292,7 +292,7 @@ template cudaError_t launch_exact<double>(const double*, int64_t, int, int, cons
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
                        int sm_count, cudaStream_t st) {
-    fix_list_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, g, P, labels, list, hdr, B);
+    fix_list_kernel<<<sm_count * 16, FX_WARPS * 32, 0, st>>>(src, g, P, labels, list, hdr, B);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fix_scan_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, batch, g, P, labels, hdr, B);
