@@ -20,6 +20,8 @@
 // The same machinery runs per row band for the multi-GPU partition
 // (trace_edges_parallel, hysteresis.py:90-131): band-edge components stay
 // pending until the cross-band merge.
+#include <algorithm>
+
 #include "ef_common.cuh"
 #include "ef_internal.h"
 
@@ -872,23 +874,30 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
 // (every perimeter slot holding its own id if a stripe overflowed).  Block 0
 // also folds the per-stripe counts into the statistics.
 __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr) {
-    const bool all = hdr->node_overflow != 0;
-    const long long n = all ? nslots : (long long)PL_STRIPES * (long long)b.node_scap;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        int node;
-        if (all) {
+    // grid (x, PL_STRIPES): blockIdx.y is the stripe; on overflow every block
+    // row scans a 1/PL_STRIPES share of the perimeter slots instead
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long first = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (hdr->node_overflow) {
+        const long long share = (nslots + PL_STRIPES - 1) / PL_STRIPES;
+        const long long lo = share * blockIdx.y, hi = min(nslots, lo + share);
+        for (long long e = lo + first; e < hi; e += stride) {
             if (!b.border[e / HP]) continue;  // perim[] of a tile without border components is stale
-            node = b.perim[e];
+            const int node = b.perim[e];
             if (node != (int)e) continue;  // the node's own (smallest) slot only
-        } else {
-            const long long stripe = e / (long long)b.node_scap, k = e - stripe * (long long)b.node_scap;
-            if (k >= (long long)b.node_count[stripe]) continue;
-            node = b.node_list[e];
+            const int r = gfind(b.gpar, node);
+            if (b.gstrong[node] && r != node) b.gstrong[r] = 1;
         }
-        const int r = gfind(b.gpar, node);
-        if (b.gstrong[node] && r != node) b.gstrong[r] = 1;
+    } else {
+        const long long n = (long long)min(b.node_count[blockIdx.y], b.node_scap);
+        const int* list = b.node_list + (long long)blockIdx.y * b.node_scap;
+        for (long long e = first; e < n; e += stride) {
+            const int node = list[e];
+            const int r = gfind(b.gpar, node);
+            if (b.gstrong[node] && r != node) b.gstrong[r] = 1;
+        }
     }
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
         unsigned long long nodes = 0, pend = 0;
         for (int i = threadIdx.x; i < PL_STRIPES; i += 32) {
             nodes += b.node_count[i];
@@ -910,13 +919,12 @@ __global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs
     // on overflow the list is incomplete (chunks past the cap were dropped) and
     // hyst_final_tile_kernel finalises every pending tile instead
     if (hdr->plist_overflow) return;
-    const unsigned long long n = (unsigned long long)PL_STRIPES * b.plist_scap;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-         e += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long stripe = e / b.plist_scap, k = e - stripe * b.plist_scap;
-        if (k >= b.plist_count[stripe]) continue;
-        if (b.gstrong[gfind_ro(b.gpar, b.plist_node[e])]) final_out[b.plist_idx[e]] = 1;
-    }
+    // grid (x, PL_STRIPES): blockIdx.y is the stripe
+    const unsigned long long n = min(b.plist_count[blockIdx.y], b.plist_scap);
+    const unsigned long long base = (unsigned long long)blockIdx.y * b.plist_scap;
+    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (unsigned long long)gridDim.x * blockDim.x)
+        if (b.gstrong[gfind_ro(b.gpar, b.plist_node[base + k])]) final_out[b.plist_idx[base + k]] = 1;
 }
 
 struct TileCCL;
@@ -1030,15 +1038,13 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
     hyst_merge_kernel<<<mgrid, 256, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    long long blocks = (L.slots + 255) / 256;
-    if (blocks > (long long)sm_count * 16) blocks = (long long)sm_count * 16;
-    hyst_resolve_kernel<<<(unsigned)blocks, 256, 0, st>>>(L.slots, b, hdr);
+    hyst_resolve_kernel<<<dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), 256, 0, st>>>(L.slots, b, hdr);
     return cudaGetLastError();
 }
 
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
-    hyst_final_list_kernel<<<sm_count * 4, 256, 0, st>>>(final_out, b, hdr);
+    hyst_final_list_kernel<<<dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), 256, 0, st>>>(final_out, b, hdr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     HystLayout L = hyst_layout(batch, H, W);
