@@ -43,7 +43,13 @@ namespace ef {
 constexpr int V2_WARPS = 4;
 constexpr int V2_THREADS = 32 * V2_WARPS;
 constexpr int V2_COLS = 128;
-constexpr int V2_TH = 32;
+#ifndef EF_K1_TH
+#define EF_K1_TH 32
+#endif
+#ifndef EF_K1_MINB
+#define EF_K1_MINB 6  // CTAs per SM the register budget is sized for (shared memory allows 6 at TH = 32)
+#endif
+constexpr int V2_TH = EF_K1_TH;  // output rows per tile
 constexpr int V2_BROWS = V2_TH + 4;
 
 constexpr int V2_MAXR = 6;
@@ -355,7 +361,11 @@ __device__ __forceinline__ void tma_stage(Smem& S, const CUtensorMap& tmap, int 
 // ---------------------------------------------------------------------------
 constexpr int V3_MROWS = V2_TH + 2;                                   // magnitude rows y0-1 .. y0+TH
 constexpr int V3_MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;          // 9 per warp
-constexpr int V3_QCAP = 64;
+#ifndef EF_K1_QCAP
+#define EF_K1_QCAP 64
+#endif
+constexpr int V3_QCAP = EF_K1_QCAP;  // >= 32; a word that would overflow waits for a flush
+static_assert(V3_QCAP >= 32 && V3_QCAP <= 64, "queue capacity");
 
 struct V3Smem {
     float b[V2_BROWS][V2_COLS];
@@ -412,15 +422,11 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     float d[3][4], sm[3][4];
     sobel_row(brow(y0 - 2 + j0), d[0], sm[0]);
     sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
-    static_assert(V3_MPW % 3 == 0, "row ring period");
-#pragma unroll 1
-    for (int u3 = 0; u3 < V3_MPW; u3 += 3)
-#pragma unroll
-    for (int u1 = 0; u1 < 3; ++u1) {
-        const int u = u3 + u1;
+    // one magnitude row; (pu, pm, pd) = ring slots of the b rows above, at and
+    // below it (period 3)
+    auto row_step = [&](int u, int pu, int pm, int pd) {
         const int j = j0 + u;
         const int Ym = y0 - 1 + j;
-        const int pu = u1, pm = (u1 + 1) % 3, pd = (u1 + 2) % 3;
         sobel_row(brow(Ym + 1), d[pd], sm[pd]);
         const float2 two = f2(2.f, 2.f);
         const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[pd][0], d[pd][1])));
@@ -446,6 +452,17 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
             if (lane == 0) S.cmask[j - 1] = b0;
         }
         lab += Wq;
+    };
+    if constexpr (V3_MPW % 3 == 0) {
+#pragma unroll 1
+        for (int u3 = 0; u3 < V3_MPW; u3 += 3) {
+            row_step(u3, 0, 1, 2);
+            row_step(u3 + 1, 1, 2, 0);
+            row_step(u3 + 2, 2, 0, 1);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < V3_MPW; ++u) row_step(u, u % 3, (u + 1) % 3, (u + 2) % 3);
     }
 }
 
@@ -459,15 +476,17 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
     unsigned nz = __ballot_sync(0xffffffffu, word != 0u);
     int qn = 0;
     while (nz || qn) {
-        if (nz) {  // append one word's pixels
+        if (nz) {  // append one word's groups if they fit, else classify first
             const int i = __ffs(nz) - 1;
-            nz &= nz - 1;
             const unsigned mask = __shfl_sync(0xffffffffu, word, i);
-            const int r = warp + V2_WARPS * i;
-            if ((mask >> lane) & 1u)
-                S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 7) | lane);
-            qn += __popc(mask);
-            if (qn < 32 && nz) continue;
+            if (qn + __popc(mask) <= V3_QCAP) {
+                nz &= nz - 1;
+                const int r = warp + V2_WARPS * i;
+                if ((mask >> lane) & 1u)
+                    S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 7) | lane);
+                qn += __popc(mask);
+                if (qn < 32 && nz) continue;
+            }
         }
         // classify 32 (or the last few) with every lane busy
         __syncwarp();
@@ -491,7 +510,7 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
 }
 
 template <int R>
-__global__ void __launch_bounds__(V2_THREADS, 6)
+__global__ void __launch_bounds__(V2_THREADS, EF_K1_MINB)
 k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
             unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
             const __grid_constant__ CUtensorMap tmap, int use_tma, FgBits B) {
