@@ -16,6 +16,7 @@
 #include "ef_common.cuh"
 #include "ef_internal.h"
 #include "ef_host.h"
+#include "ef_launch.cuh"
 
 using namespace ef;
 
@@ -140,7 +141,16 @@ Ws ws_bind(void* base, const WsLayout& L) {
     return w;
 }
 
-__global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs hb) {
+// Resets the per-call workspace state; with `planes` (the fused path) also
+// zeroes the two foreground bit planes (2 * nwords words).
+__global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs hb, unsigned long long* planes,
+                                unsigned long long nwords) {
+    pdl_wait();  // the previous call's kernels on this stream read the same workspace
+    pdl_trigger();
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        planes[i] = 0ull;
+    if (blockIdx.x != 0) return;
     if (threadIdx.x == 0) {
         hdr->fix_count = 0;
         hdr->fix_cap = cap;
@@ -154,6 +164,12 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs 
         hb.node_count[threadIdx.x] = 0;
         hb.pend_tiles[threadIdx.x] = 0;
     }
+}
+
+cudaError_t launch_ws_begin(const Ws& ws, const WsLayout& L, unsigned long long nwords, int sms, cudaStream_t st) {
+    const unsigned long long want = (nwords + 255) / 256;
+    const unsigned blocks = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, 4ull * sms));
+    return launch_pdl(ws_begin_kernel, dim3(blocks), dim3(256), 0, st, ws.hdr, L.fix_cap, ws.hb, ws.fgbits, nwords);
 }
 
 __global__ void ws_reset_stats_kernel(WsHeader* hdr) {
@@ -272,20 +288,17 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
                  "exact kernel");
         return EF_OK;
     }
-    ws_begin_kernel<<<1, PL_STRIPES, 0, st>>>(ws.hdr, L.fix_cap, ws.hb);
-    EF_CHECK(cudaGetLastError(), "ws_begin");
     FastParams FP = make_fast(w, r, low, high);
     FgBits B{};
+    unsigned long long nwords = 0;  // bit-plane words ws_begin zeroes (both planes and the gap between)
     static const bool no_bits = getenv("EF_NO_FG_BITS") != nullptr;  // A/B switch for profiling
     if (fin && bits && !no_bits && k1_emits_bits(FP, g)) {
         const int words = (g.W + 63) / 64;
         B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)g.rows * words};
-        const size_t plane = (size_t)batch * g.rows * words * sizeof(unsigned long long);
-        EF_CHECK(cudaMemsetAsync(ws.fgbits, 0, plane, st), "bit planes");
-        EF_CHECK(cudaMemsetAsync(ws.stbits, 0, plane, st), "bit planes");
-
+        nwords = (unsigned long long)(ws.stbits - ws.fgbits) + (unsigned long long)batch * g.rows * words;
         *bits = B;
     }
+    EF_CHECK(launch_ws_begin(ws, L, nwords, sms, st), "ws_begin");
     const Timing& T = timing();
     if (T.start) EF_CHECK(cudaEventRecord(T.start, st), "timing event");
     EF_CHECK(launch_k1(src, batch, g, FP, labels, ws.fix, ws.hdr, B, st), "classify kernel");
@@ -300,10 +313,7 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
               cudaStream_t st, bool finalize, bool reset, const FgBits* bits = nullptr) {
     const int sms = sm_count_current();
-    if (reset) {
-        ws_begin_kernel<<<1, PL_STRIPES, 0, st>>>(ws.hdr, L.fix_cap, ws.hb);
-        EF_CHECK(cudaGetLastError(), "ws_begin");
-    }
+    if (reset) EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");
     if (bits && !bits->fg) bits = nullptr;
     EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, bits, sms, st), "hysteresis");
     if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");

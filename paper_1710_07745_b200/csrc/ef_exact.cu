@@ -16,6 +16,7 @@
 // every read of the previous stage clamps its coordinates into the image.
 #include "ef_common.cuh"
 #include "ef_internal.h"
+#include "ef_launch.cuh"
 
 namespace ef {
 
@@ -222,6 +223,8 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
                 const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5;
     unsigned long long n = hdr->fix_count;
     if (n > hdr->fix_cap) n = hdr->fix_cap;
@@ -243,6 +246,8 @@ fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, Exa
                 uint8_t* labels, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
+    pdl_wait();
+    pdl_trigger();
     if (!hdr->overflow) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned long long total = (unsigned long long)batch * g.rows * g.W;
@@ -292,11 +297,11 @@ template cudaError_t launch_exact<double>(const double*, int64_t, int, int, cons
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
                        int sm_count, cudaStream_t st) {
-    fix_list_kernel<<<sm_count * 16, FX_WARPS * 32, 0, st>>>(src, g, P, labels, list, hdr, B);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(fix_list_kernel, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, g, P, labels,
+                               list, hdr, B);
     if (e != cudaSuccess) return e;
-    fix_scan_kernel<<<sm_count * 4, FX_WARPS * 32, 0, st>>>(src, batch, g, P, labels, hdr, B);
-    return cudaGetLastError();
+    return launch_pdl(fix_scan_kernel, dim3(sm_count * 4), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, hdr,
+                      B);
 }
 
 }  // namespace ef

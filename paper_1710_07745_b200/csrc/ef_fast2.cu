@@ -37,6 +37,7 @@
 
 #include "ef_common.cuh"
 #include "ef_internal.h"
+#include "ef_launch.cuh"
 
 namespace ef {
 
@@ -516,6 +517,8 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             const __grid_constant__ CUtensorMap tmap, int use_tma, FgBits B) {
     extern __shared__ __align__(16) unsigned char smraw[];
     V3Smem& S = *reinterpret_cast<V3Smem*>(smraw);
+    pdl_wait();  // workspace counters and bit planes are reset by the previous kernel
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x0 = blockIdx.x * V2Cfg<R>::OW;
     const int xv0 = x0 - V2Cfg<R>::HXA;
@@ -601,8 +604,7 @@ static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& 
     CUtensorMap tm;
     std::memset(&tm, 0, sizeof tm);
     const int use_tma = make_src_map(tm, src, batch, g, R) && !getenv("EF_NO_TMA");
-    kern<<<grid, V2_THREADS, smem, st>>>(src, g, P, labels, fix_list, hdr, tm, use_tma, B);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, dim3(V2_THREADS), (size_t)smem, st, src, g, P, labels, fix_list, hdr, tm, use_tma, B);
 }
 
 cudaError_t launch_k1v2(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,

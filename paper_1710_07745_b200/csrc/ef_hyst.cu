@@ -24,6 +24,7 @@
 
 #include "ef_common.cuh"
 #include "ef_internal.h"
+#include "ef_launch.cuh"
 
 namespace ef {
 
@@ -464,6 +465,8 @@ __global__ void __launch_bounds__(H_THREADS)
 hyst_dense_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
                   uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
     __shared__ TileCCL s;
+    pdl_wait();
+    pdl_trigger();
     const unsigned n = hdr->dense_count;
     for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
         const long long tile = b.dense[e];
@@ -552,6 +555,8 @@ __global__ void __launch_bounds__(32 * WT_WARPS)
 hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
                        uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr, FgBits B) {
     __shared__ WarpTile tiles[WT_WARPS];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tpf = tiles_x * tiles_y;
     const int t = blockIdx.x * WT_WARPS + warp;
@@ -817,6 +822,8 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
 // and seams whose other side has none -- are skipped on one byte.
 __global__ void __launch_bounds__(256)
 hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tpf = tiles_x * tiles_y;
     const int t = blockIdx.x * 8 + warp;
@@ -874,6 +881,8 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
 // (every perimeter slot holding its own id if a stripe overflowed).  Block 0
 // also folds the per-stripe counts into the statistics.
 __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr) {
+    pdl_wait();
+    pdl_trigger();
     // grid (x, PL_STRIPES): blockIdx.y is the stripe; on overflow every block
     // row scans a 1/PL_STRIPES share of the perimeter slots instead
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -916,6 +925,8 @@ __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr)
 
 // H4: pixels of undecided border components read their root's strong flag.
 __global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
+    pdl_wait();
+    pdl_trigger();
     // on overflow the list is incomplete (chunks past the cap were dropped) and
     // hyst_final_tile_kernel finalises every pending tile instead
     if (hdr->plist_overflow) return;
@@ -937,6 +948,8 @@ __global__ void __launch_bounds__(H_THREADS)
 hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, int frames,
                        uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
     __shared__ TileCCL s;
+    pdl_wait();
+    pdl_trigger();
     if (!hdr->plist_overflow) return;
     const long long ntiles = (long long)tiles_x * tiles_y * frames;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1023,33 +1036,33 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
     cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     const dim3 wgrid((unsigned)((L.tiles_x * L.tiles_y + WT_WARPS - 1) / WT_WARPS), (unsigned)batch);
+    cudaError_t e;
     if (bits)
-        hyst_local_warp_kernel<true><<<wgrid, 32 * WT_WARPS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
-                                                                     b, hdr, *bits);
+        e = launch_pdl(hyst_local_warp_kernel<true>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
+                       L.tiles_y, final_out, b, hdr, *bits);
     else
-        hyst_local_warp_kernel<false><<<wgrid, 32 * WT_WARPS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out,
-                                                                      b, hdr, FgBits{});
-    cudaError_t e = cudaGetLastError();
+        e = launch_pdl(hyst_local_warp_kernel<false>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
+                       L.tiles_y, final_out, b, hdr, FgBits{});
     if (e != cudaSuccess) return e;
-    hyst_dense_kernel<<<sm_count * 4, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, final_out, b, hdr);
-    e = cudaGetLastError();
+    e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x, L.tiles_y,
+                   final_out, b, hdr);
     if (e != cudaSuccess) return e;
     const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);
-    hyst_merge_kernel<<<mgrid, 256, 0, st>>>(H, W, L.tiles_x, L.tiles_y, b);
-    e = cudaGetLastError();
+    e = launch_pdl(hyst_merge_kernel, mgrid, dim3(256), 0, st, H, W, L.tiles_x, L.tiles_y, b);
     if (e != cudaSuccess) return e;
-    hyst_resolve_kernel<<<dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), 256, 0, st>>>(L.slots, b, hdr);
-    return cudaGetLastError();
+    return launch_pdl(hyst_resolve_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), dim3(256), 0, st,
+                      (long long)L.slots, b, hdr);
 }
 
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
-    hyst_final_list_kernel<<<dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), 256, 0, st>>>(final_out, b, hdr);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(hyst_final_list_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES),
+                               dim3(256), 0, st, final_out, b, hdr);
     if (e != cudaSuccess) return e;
     HystLayout L = hyst_layout(batch, H, W);
-    hyst_final_tile_kernel<<<sm_count * 2, H_THREADS, 0, st>>>(labels, H, W, L.tiles_x, L.tiles_y, (int)batch,
-                                                               final_out, b, hdr);
+    e = launch_pdl(hyst_final_tile_kernel, dim3(sm_count * 2), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x,
+                   L.tiles_y, (int)batch, final_out, b, hdr);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
