@@ -294,7 +294,8 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     static const bool no_bits = getenv("EF_NO_FG_BITS") != nullptr;  // A/B switch for profiling
     if (fin && bits && !no_bits && k1_emits_bits(FP, g)) {
         const int words = (g.W + 63) / 64;
-        B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)g.rows * words};
+        B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)g.rows * words,
+                   (long long)(reinterpret_cast<intptr_t>(fin) - reinterpret_cast<intptr_t>(labels))};
         nwords = (unsigned long long)(ws.stbits - ws.fgbits) + (unsigned long long)batch * g.rows * words;
         *bits = B;
     }

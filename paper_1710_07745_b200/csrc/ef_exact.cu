@@ -211,8 +211,10 @@ __device__ __forceinline__ void out_coords(unsigned long long idx, const FrameGe
 
 // the fused pipeline's foreground bit planes for a fixed pixel
 __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, unsigned long long f, int y, int x,
-                                         uint8_t lab) {
-    if (!B.fg || (threadIdx.x & 31) != 0 || (lab != 1 && lab != 2)) return;
+                                         uint8_t lab, uint8_t* lab_ptr) {
+    if (!B.fg || (threadIdx.x & 31) != 0) return;
+    lab_ptr[B.fin_off] = lab == 2 ? 1 : 0;  // final = strong (weak pixels are decided by the hysteresis)
+    if (lab != 1 && lab != 2) return;
     const unsigned long long w = f * B.frame_words + (unsigned long long)(y - g.out0) * B.words + (unsigned)(x >> 6);
     atomicOr(&B.fg[w], 1ull << (x & 63));
     if (lab == 2) atomicOr(&B.st[w], 1ull << (x & 63));
@@ -235,7 +237,7 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
         out_coords(idx, g, f, y, x);
         fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
                        labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
-        fix_bits(B, g, f, y, x, labels[idx]);
+        fix_bits(B, g, f, y, x, labels[idx], labels + idx);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)&hdr->stats.fixups, hdr->fix_count);
 }
@@ -264,7 +266,7 @@ fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, Exa
             out_coords(p, g, f, y, x);
             fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
                            labels + p, (unsigned long long*)&hdr->stats.ambiguous);
-            fix_bits(B, g, f, y, x, labels[p]);
+            fix_bits(B, g, f, y, x, labels[p], labels + p);
         }
     }
 }

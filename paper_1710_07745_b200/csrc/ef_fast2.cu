@@ -310,6 +310,8 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
     }
     *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
     if (bits.fg) {
+        // final = strong (kFlag bytes give 0: the fix-up writes them)
+        *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0 + bits.fin_off) = (packed >> 1) & 0x01010101u;
         // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
         const uint32_t lo = packed & 0x03030303u;
         const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;
@@ -420,6 +422,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         return &S.b[(INTERIOR ? Y : clampi(Y, 0, FH - 1)) - (y0 - 2)][l];
     };
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
+    const long long fin_off = S.bits.fg ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
     float d[3][4], sm[3][4];
     sobel_row(brow(y0 - 2 + j0), d[0], sm[0]);
     sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
@@ -448,7 +451,10 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         if (j >= 1 && j <= V2_TH) {
             const bool act = out_lane && (INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH));
             const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
-            if (act && !cand) *lab = fill;
+            if (act && !cand) {
+                *lab = fill;
+                if (fin_off) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
+            }
             const unsigned b0 = __ballot_sync(0xffffffffu, cand);
             if (lane == 0) S.cmask[j - 1] = b0;
         }

@@ -547,8 +547,9 @@ __device__ __forceinline__ int row_of(const WarpTile& s, int e) {
 }
 
 // BITS: the fused pipeline -- the classifier ORed the foreground / strong
-// pixels into bit planes, so a tile reads 2 bits per pixel instead of its
-// label bytes.  Either way the whole final tile is written.
+// pixels into bit planes and wrote final = strong, so a tile reads 2 bits per
+// pixel instead of its label bytes and stores only weak pixels that join an
+// edge.  Otherwise the label bytes are read and the whole final tile written.
 // Grid: (ceil(tiles per frame / WT_WARPS), frames); one warp per tile.
 template <bool BITS>
 __global__ void __launch_bounds__(32 * WT_WARPS)
@@ -702,7 +703,9 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
                 pix = s.list[e];
                 v = s.info[s.par[e]];
                 if (info_strong(v)) {
-                    atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
+                    if (!BITS) atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
+                    else if (!((s.strow[pix >> 6] >> (pix & (HT - 1))) & 1ull))  // weak pixel joins an edge
+                        final_out[frame_off + (size_t)(g.y0 + (pix >> 6)) * W + g.x0 + (pix & (HT - 1))] = 1;
                 } else {
                     pend = info_slot(v) != NO_SLOT;
                 }
@@ -725,9 +728,10 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
         __syncwarp();
     }
-    {
-        // ---- whole final tile (4 lanes per row, 16 bytes each): one pass
-        // writes the zeros too (cheaper than a memset of final before K1)
+    if (!BITS) {
+        // ---- whole final tile (4 lanes per row, 16 bytes each).  (BITS: the
+        // classifier wrote final = strong for every pixel; only the weak
+        // pixels joining an edge are stored above.)
         const bool full_out = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(final_out) & 15) == 0);
 #pragma unroll 2
         for (int it = 0; it < HT / 8; ++it) {

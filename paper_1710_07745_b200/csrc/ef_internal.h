@@ -54,6 +54,7 @@ struct FgBits {
     unsigned long long* st;
     int words;                     // words per output row: ceil(W / 64)
     unsigned long long frame_words;  // words per frame: rows * words
+    long long fin_off;             // final map - label map (bytes): the classifier also writes final = strong
 };
 
 #ifdef __CUDACC__
