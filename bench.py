@@ -366,7 +366,10 @@ def run_ours(args):
                        "cross PCIe packed to 2 bits/px and are expanded into the host arrays by a host thread pool)"}
 
     peak, peak_kind = peaks()
-    alg_bytes = 2 * px  # u8 in + class byte out per pixel
+    # algorithmic bytes of the roofline kernel: u8 in + label byte out (SURVEY 8d's
+    # 2 B/px) + the final byte the fused K1 also writes (final = strong; the
+    # hysteresis only adds the weak pixels that join an edge) = 3 B/px
+    alg_bytes = 3 * px
     achieved = alg_bytes / (k1_ms / 1e3) / 1e9
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(frames, w, low, high)
@@ -385,7 +388,11 @@ def run_ours(args):
                          "traffic": ncu_traffic() if (args.config == 1 and b == 64 and args.radius == 2) else None,
                          "traffic_source": "profiles/r01_k1v3_dram_64frames.csv (ncu dram__bytes_read+write per launch)",
                          "peak_kind": peak_kind,
-                         "alg_bytes_per_launch": int(alg_bytes), "avg_launch_ms": round(k1_ms, 4),
+                         "alg_bytes_per_launch": int(alg_bytes),
+                         "alg_bytes_note": "3 B/px: u8 in, label out, final out (K1 writes final = strong in the "
+                                           "fused path); SURVEY 8d's classify-only figure is 2 B/px",
+                         "frac_at_2bpx": round(achieved * 2 / 3 / peak, 4),
+                         "avg_launch_ms": round(k1_ms, 4),
                          "share_of_step": round(k1_ms / ms, 3)},
             "e2e": e2e,
             "cpu_baseline": cpu,
