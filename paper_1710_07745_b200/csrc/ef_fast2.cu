@@ -566,16 +566,15 @@ bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 &
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // thread-safe one-time lookup (function-local static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult q;
         void* p = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return nullptr;
+    }();
     return fn;
 }
 
@@ -600,11 +599,15 @@ static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& 
                             cudaStream_t st) {
     auto kern = k1v3_kernel<R>;
     const int smem = (int)sizeof(V3Smem);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    // occupancy is shared-memory bound: ask for the largest carveout
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
+    static std::atomic<uint64_t> configured{0};
+    cudaError_t e = once_per_device(configured, [&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        // occupancy is shared-memory bound: ask for the largest carveout
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
+        return r;
+    });
     if (e != cudaSuccess) return e;
     dim3 grid((g.W + V2Cfg<R>::OW - 1) / V2Cfg<R>::OW, (g.rows + V2_TH - 1) / V2_TH, (unsigned)batch);
     CUtensorMap tm;

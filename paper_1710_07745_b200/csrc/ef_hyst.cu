@@ -1032,15 +1032,18 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                               const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
                               cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    cudaFuncSetAttribute(hyst_local_warp_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
     // shared memory bound (5 KB per warp tile, 20 KB per dense tile): full carveout
-    cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
+    static std::atomic<uint64_t> configured{0};
+    cudaError_t e = once_per_device(configured, [] {
+        const int c = (int)cudaSharedmemCarveoutMaxShared;
+        cudaError_t r = cudaFuncSetAttribute(hyst_local_warp_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+        return r;
+    });
+    if (e != cudaSuccess) return e;
     const dim3 wgrid((unsigned)((L.tiles_x * L.tiles_y + WT_WARPS - 1) / WT_WARPS), (unsigned)batch);
-    cudaError_t e;
     if (bits)
         e = launch_pdl(hyst_local_warp_kernel<true>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
                        L.tiles_y, final_out, b, hdr, *bits);

@@ -13,6 +13,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <utility>
 
@@ -24,6 +26,21 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 inline bool pdl_enabled() {
     static const bool on = getenv("EF_NO_PDL") == nullptr;  // A/B switch
     return on;
+}
+
+// Function attributes are per device; set them once per (call site, device)
+// instead of on every launch (each cudaFuncSetAttribute is a driver call).
+// `done` is a per-call-site bit set of devices already configured.
+template <typename F>
+cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 template <typename... KArgs, typename... Args>
