@@ -91,7 +91,7 @@ def _random_image(rng, h, w, kind):
     return ((x * 7 + y * 3) % 256).astype(np.uint8)
 
 
-@pytest.mark.parametrize("r", [0, 1, 2, 3, 5, 8, 15])
+@pytest.mark.parametrize("r", [0, 1, 2, 3, 4, 5, 6, 7, 8, 15])
 def test_fast_path_random_vs_oracle(canny, r):
     rng = np.random.default_rng(100 + r)
     sigma = max(0.3, r / 3.0)
