@@ -41,7 +41,10 @@
 
 namespace ef {
 
-constexpr int V2_WARPS = 4;
+#ifndef EF_K1_WARPS
+#define EF_K1_WARPS 4
+#endif
+constexpr int V2_WARPS = EF_K1_WARPS;
 constexpr int V2_THREADS = 32 * V2_WARPS;
 constexpr int V2_COLS = 128;
 #ifndef EF_K1_TH
@@ -479,7 +482,8 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
     const int FH = P.FH;
     // this warp's 8 candidate words (rows warp + 4 i), one per lane; only
     // non-empty words are visited
-    const unsigned word = lane < V2_TH / V2_WARPS ? S.cmask[warp + V2_WARPS * lane] : 0u;
+    const int wrow = warp + V2_WARPS * lane;
+    const unsigned word = (lane < (V2_TH + V2_WARPS - 1) / V2_WARPS && wrow < V2_TH) ? S.cmask[wrow] : 0u;
     unsigned nz = __ballot_sync(0xffffffffu, word != 0u);
     int qn = 0;
     while (nz || qn) {
@@ -551,10 +555,10 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         // magnitude rows -1 and FH replicate rows 0 and FH-1 (np.pad edge)
         const int FH = g.full_H;
         if (y0 - 1 < 0 || y0 + V2_TH >= FH) {
-            const int t = threadIdx.x;  // 128 threads = one row of 128 columns
-            if (y0 - 1 < 0) S.m[0][t] = S.m[1][t];
+            const int t = threadIdx.x;  // the first 128 threads copy one row of 128 columns
+            if (t < V2_COLS && y0 - 1 < 0) S.m[0][t] = S.m[1][t];
             const int jf = FH - (y0 - 1);  // tile row of Ym = FH
-            if (jf >= 1 && jf < V3_MROWS) S.m[jf][t] = S.m[jf - 1][t];
+            if (t < V2_COLS && jf >= 1 && jf < V3_MROWS) S.m[jf][t] = S.m[jf - 1][t];
             __syncthreads();
         }
     }
