@@ -134,6 +134,26 @@ def test_fused_foreground_lists_vs_two_call_path(canny, density):
         assert np.array_equal(_np(fin2).astype(bool), ef_), (density, b, h, wd)
 
 
+def test_workspace_reuse_across_inputs_and_shapes(canny):
+    """One workspace, dirtied by a dense noise batch, reused for smaller and
+    differently shaped sparse batches (stale perimeter slots, bit planes and list
+    counters must never leak into a later call), and by the two-call path."""
+    import torch
+    rng = np.random.default_rng(11)
+    w = O.gaussian_weights(1.4, radius=2)
+    big = (3, 256, 320)
+    ws = torch.full((canny.new_workspace(*big).numel(),), 0xA5, dtype=torch.uint8, device="cuda")
+    cases = [rng.integers(0, 256, size=big, dtype=np.uint8), synth.config1(2, 130, 200), synth.config1(3, 256, 320),
+             synth.config1(1, 64, 64), rng.integers(0, 256, size=(2, 200, 96), dtype=np.uint8)]
+    for frames in cases:
+        el, ef_ = O.canny(frames, w, 20.0, 50.0)
+        lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0, ws=ws)
+        assert np.array_equal(_np(lab), el) and np.array_equal(_np(fin).astype(bool), ef_), frames.shape
+        lab2 = canny.classify_u8(_dev(frames), w, 20.0, 50.0, ws=ws)
+        fin2 = canny.trace_edges_u8(lab2, ws=ws)
+        assert np.array_equal(_np(fin2).astype(bool), ef_), frames.shape
+
+
 def test_float_path_random_vs_oracle(canny):
     rng = np.random.default_rng(5)
     for (h, wd) in [(1, 1), (7, 5), (33, 47), (128, 96)]:
