@@ -115,6 +115,34 @@ void flush_lines(const uint8_t* p, size_t n) {
     _mm_mfence();
 }
 
+// AVX2 + BMI2 body: 8 packed bytes (32 pixels) per step.  pdep spreads each
+// 2-bit code into a byte; label = (code + 1) >> 1 and final = code >> 1 bytewise
+// (codes <= 3, so no carries cross bytes); two 32-byte non-temporal stores.
+// Returns the first packed byte not done; labels + 4*j must be 32-byte aligned.
+__attribute__((target("avx2,bmi2"))) static size_t unpack_avx2(const uint8_t* packed, size_t j, size_t end,
+                                                                uint8_t* labels, uint8_t* final_map) {
+    const __m256i one = _mm256_set1_epi8(1), low7 = _mm256_set1_epi8(0x7f);
+    for (; j + 8 <= end; j += 8) {
+        uint64_t w;
+        std::memcpy(&w, packed + j, 8);
+        const __m256i codes = _mm256_setr_epi64x(
+            (long long)_pdep_u64(w & 0xffffu, 0x0303030303030303ull),
+            (long long)_pdep_u64((w >> 16) & 0xffffu, 0x0303030303030303ull),
+            (long long)_pdep_u64((w >> 32) & 0xffffu, 0x0303030303030303ull),
+            (long long)_pdep_u64((w >> 48) & 0xffffu, 0x0303030303030303ull));
+        const __m256i lab = _mm256_and_si256(_mm256_srli_epi16(_mm256_add_epi8(codes, one), 1), low7);
+        const __m256i fin = _mm256_and_si256(_mm256_srli_epi16(codes, 1), one);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(labels + 4 * j), lab);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(final_map + 4 * j), fin);
+    }
+    return j;
+}
+
+static bool has_avx2_bmi2() {
+    static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("bmi2");
+    return ok;
+}
+
 void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx, uint8_t* labels,
                   uint8_t* final_map) {
     const Luts& T = luts();
@@ -126,6 +154,12 @@ void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx,
         std::memcpy(labels + 4 * b, &l, 4);
         std::memcpy(final_map + 4 * b, &f, 4);
     };
+    const bool same_phase32 = ((reinterpret_cast<uintptr_t>(labels) ^ reinterpret_cast<uintptr_t>(final_map)) & 31) == 0;
+    if (same_phase32 && has_avx2_bmi2()) {
+        while (j < full_end && (reinterpret_cast<uintptr_t>(labels + 4 * j) & 31)) scalar(j++);
+        j = unpack_avx2(packed, j, full_end, labels, final_map);
+        _mm_sfence();
+    }
     const bool same_phase = ((reinterpret_cast<uintptr_t>(labels) ^ reinterpret_cast<uintptr_t>(final_map)) & 15) == 0;
     if (same_phase) {
         while (j < full_end && (reinterpret_cast<uintptr_t>(labels + 4 * j) & 15)) scalar(j++);

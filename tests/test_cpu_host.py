@@ -158,3 +158,20 @@ def test_no_cpu_fallback():
         ef.run_pipeline(img, ef.PipelineConfig(thresholds=ef.Thresholds(1.0, 2.0)))
     with pytest.raises(RuntimeError, match="CUDA"):
         ef.trace_edges(ef.EdgeMap(width=1, height=1, labels=np.zeros((1, 1), np.uint8)))
+
+
+def test_unpack_codes_matches_scalar_decode(tmp_path):
+    """The host unpack of the packed (labels, final) stream (SIMD and scalar
+    paths, every alignment) -- compiled against the built library."""
+    import shutil
+    import subprocess
+    from paper_1710_07745_b200 import build as B
+
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    lib = B.build()
+    exe = tmp_path / "unpack_check"
+    src = os.path.join(os.path.dirname(__file__), "native", "unpack_check.cpp")
+    subprocess.run(["g++", "-O2", "-o", str(exe), src, lib, f"-Wl,-rpath,{os.path.dirname(lib)}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert "unpack ok" in out
