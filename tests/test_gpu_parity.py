@@ -154,6 +154,50 @@ def test_workspace_reuse_across_inputs_and_shapes(canny):
         assert np.array_equal(_np(fin2).astype(bool), ef_), frames.shape
 
 
+@pytest.mark.parametrize("low,high", [(5.0, 100.0), (2.0, 400.0)])
+def test_dense_noise_overflow_paths(canny, low, high):
+    """Dense noise with low thresholds: tiles beyond the warp kernel's capacity
+    (block-kernel path), node and pending-list stripes that overflow (perimeter
+    scan / tile re-run fallbacks) -- all must still equal the oracle."""
+    rng = np.random.default_rng(int(low * 10 + high))
+    frames = rng.integers(0, 256, size=(1, 2048, 2048), dtype=np.uint8)
+    w = O.gaussian_weights(0.6, radius=1)
+    el, ef_ = O.canny(frames, w, low, high)
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+    lab2 = canny.classify_u8(_dev(frames), w, low, high)
+    assert np.array_equal(_np(canny.trace_edges_u8(lab2)).astype(bool), ef_)
+
+
+@pytest.mark.parametrize("low,high", [(48.0, 48.0), (16.0, 48.0)])
+def test_fix_list_overflow_on_threshold_ties(canny, low, high):
+    """Binary blocks with a dyadic kernel make magnitudes exactly 16, 48, ...:
+    thresholds on those values put ~13% of the pixels inside the certification
+    bands (and NMS plateaus), far more than the fix list holds -- the full-scan
+    fix-up must still reproduce the reference exactly."""
+    rng = np.random.default_rng(3)
+    blk = rng.choice(np.array([0, 16], np.uint8), size=(512, 512))
+    frames = np.kron(blk, np.ones((4, 4), np.uint8))[None]
+    w = np.array([0.25, 0.5, 0.25])
+    el, ef_ = O.canny(frames, w, low, high)
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+
+
+def test_node_list_overflow_large_noise(canny):
+    """8192^2 noise: border components per node-list stripe beyond capacity
+    (the resolve pass falls back to scanning every perimeter slot)."""
+    rng = np.random.default_rng(8192)
+    frames = rng.integers(0, 256, size=(1, 8192, 8192), dtype=np.uint8)
+    w = O.gaussian_weights(0.6, radius=1)
+    el, ef_ = O.canny(frames, w, 5.0, 60.0)
+    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0)
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+
+
 def test_float_path_random_vs_oracle(canny):
     rng = np.random.default_rng(5)
     for (h, wd) in [(1, 1), (7, 5), (33, 47), (128, 96)]:
