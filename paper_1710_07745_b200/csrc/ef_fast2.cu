@@ -451,16 +451,17 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         *reinterpret_cast<float4*>(&S.m[j][l]) = make_float4(m01.x, m01.y, m23.x, m23.y);
         // output rows: groups certainly below `low` get the background class
         // now, the others are marked for the classifier
-        if (j >= 1 && j <= V2_TH) {
-            const bool act = out_lane && (INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH));
-            const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
-            if (act && !cand) {
-                *lab = fill;
-                if (fin_off) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
-            }
-            const unsigned b0 = __ballot_sync(0xffffffffu, cand);
-            if (lane == 0) S.cmask[j - 1] = b0;
+        // (straight-line: the vote runs on every row, the stores are predicated,
+        // so no divergent region surrounds the vote)
+        const bool outrow = j >= 1 && j <= V2_TH;
+        const bool act = outrow && out_lane && (INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH));
+        const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
+        const unsigned b0 = __ballot_sync(0xffffffffu, cand);
+        if (act && !cand) {
+            *lab = fill;
+            if (fin_off) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
         }
+        if (lane == 0 && outrow) S.cmask[j - 1] = b0;
         lab += Wq;
     };
     if constexpr (V3_MPW % 3 == 0) {
