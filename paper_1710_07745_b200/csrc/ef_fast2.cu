@@ -414,6 +414,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     // twice, with identical values, labels and candidate words.
     const int j0 = min(warp * V3_MPW, V3_MROWS - V3_MPW);
     const int oy0 = g.out0, oy1 = g.out0 + g.rows;
+    const int ylim = min(oy1, FH);  // rows at or past this are not classified here
     const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
     const int c = xv0 + 4 * lane;
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
@@ -454,7 +455,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         // (straight-line: the vote runs on every row, the stores are predicated,
         // so no divergent region surrounds the vote)
         const bool outrow = j >= 1 && j <= V2_TH;
-        const bool act = outrow && out_lane && (INTERIOR || (Ym >= oy0 && Ym < oy1 && Ym < FH));
+        const bool act = outrow && out_lane && Ym < ylim && (INTERIOR || Ym >= oy0);
         const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
         const unsigned b0 = __ballot_sync(0xffffffffu, cand);
         if (act && !cand) {
@@ -521,6 +522,33 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
     }
 }
 
+// Edge tiles on the TMA path: the box reads zeros outside the buffer, so the
+// staged input, then the blurred tile, then the magnitude tile are completed
+// in shared memory by replicating their edge rows / columns (np.pad edge at
+// every stage, the reference's border policy) -- after which the interior code
+// runs unchanged.  Columns first, then rows (corners = corner pixel).
+template <int NROWS, int NCOLS, class T>
+__device__ __forceinline__ void replicate_edges(T (*a)[NCOLS], int c_lo, int c_hi, int r_lo, int r_hi) {
+    // only the out-of-frame margins are touched: one row per thread, then one
+    // column per thread
+    if (c_lo > 0 || c_hi < NCOLS - 1) {
+        for (int r = threadIdx.x; r < NROWS; r += blockDim.x) {
+            const T vl = a[r][c_lo], vr = a[r][c_hi];
+            for (int c = 0; c < c_lo; ++c) a[r][c] = vl;
+            for (int c = c_hi + 1; c < NCOLS; ++c) a[r][c] = vr;
+        }
+        __syncthreads();
+    }
+    if (r_lo > 0 || r_hi < NROWS - 1) {
+        for (int c = threadIdx.x; c < NCOLS; c += blockDim.x) {
+            const T vt = a[r_lo][c], vb = a[r_hi][c];
+            for (int r = 0; r < r_lo; ++r) a[r][c] = vt;
+            for (int r = r_hi + 1; r < NROWS; ++r) a[r][c] = vb;
+        }
+        __syncthreads();
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(V2_THREADS, EF_K1_MINB)
 k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
@@ -539,15 +567,31 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (threadIdx.x == 0) S.bits = B;
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
-    // interior tiles take the TMA-staged fast path; without TMA (W % 16 != 0)
-    // every tile takes the general path -- one interior variant less keeps the
-    // kernel's hot code inside the instruction cache
-    if (interior && use_tma) {
+    // with TMA (W % 16 == 0) every tile takes the fast path -- edge tiles after
+    // completing their halos in shared memory; without TMA every tile takes the
+    // general path (one fast variant keeps the hot code in the instruction cache)
+    if (use_tma) {
         tma_stage<R>(S, tmap, xv0, y0, g);
+        const int FH = g.full_H, W = g.W;
+        if (!interior) {
+            // staged input: row r <-> frame row y0-2-R+r, column c <-> x = (xv0 & ~15) + c
+            constexpr int NIN = V2_BROWS + 2 * R;
+            const int xa = xv0 & ~15, yin = y0 - 2 - R;
+            const int ylo = max(0, g.g0), yhi = min(FH, g.g0 + g.H) - 1;
+            __syncthreads();
+            replicate_edges<NIN, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
+                                             max(0, ylo - yin), min(NIN - 1, yhi - yin));
+        }
         v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
+        if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
+            replicate_edges<V2_BROWS, V2_COLS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+                                               max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
         v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
         __syncthreads();
+        if (!interior)  // magnitudes: row j <-> frame row y0-1+j
+            replicate_edges<V3_MROWS, V2_COLS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+                                               max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
     } else {
         v2_phase1<R, false, false>(img, g, xv0, y0, P, S, warp, lane);
         __syncthreads();
