@@ -567,46 +567,53 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (threadIdx.x == 0) S.bits = B;
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;
-    // with TMA (W % 16 == 0) every tile takes the fast path -- edge tiles after
-    // completing their halos in shared memory; without TMA every tile takes the
-    // general path (one fast variant keeps the hot code in the instruction cache)
-    if (use_tma) {
-        tma_stage<R>(S, tmap, xv0, y0, g);
-        const int FH = g.full_H, W = g.W;
-        if (!interior) {
-            // staged input: row r <-> frame row y0-2-R+r, column c <-> x = (xv0 & ~15) + c
-            constexpr int NIN = V2_BROWS + 2 * R;
-            const int xa = xv0 & ~15, yin = y0 - 2 - R;
-            const int ylo = max(0, g.g0), yhi = min(FH, g.g0 + g.H) - 1;
-            __syncthreads();
-            replicate_edges<NIN, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
-                                             max(0, ylo - yin), min(NIN - 1, yhi - yin));
-        }
-        v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
-        __syncthreads();
-        if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
-            replicate_edges<V2_BROWS, V2_COLS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                               max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
-        v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
-        __syncthreads();
-        if (!interior)  // magnitudes: row j <-> frame row y0-1+j
-            replicate_edges<V3_MROWS, V2_COLS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                               max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
-    } else {
-        v2_phase1<R, false, false>(img, g, xv0, y0, P, S, warp, lane);
-        __syncthreads();
-        v3_phase2a<R, false>(g, xv0, y0, P, S, warp, lane, O);
-        __syncthreads();
-        // magnitude rows -1 and FH replicate rows 0 and FH-1 (np.pad edge)
-        const int FH = g.full_H;
-        if (y0 - 1 < 0 || y0 + V2_TH >= FH) {
-            const int t = threadIdx.x;  // the first 128 threads copy one row of 128 columns
-            if (t < V2_COLS && y0 - 1 < 0) S.m[0][t] = S.m[1][t];
-            const int jf = FH - (y0 - 1);  // tile row of Ym = FH
-            if (t < V2_COLS && jf >= 1 && jf < V3_MROWS) S.m[jf][t] = S.m[jf - 1][t];
+    // one code path for every tile: the input tile + halo is staged in shared
+    // memory (TMA when W % 16 == 0, else clamped loads); edge tiles complete
+    // their halos there by replication, so phases 1-3 never clamp
+    const int FH = g.full_H, W = g.W;
+    {
+        // staged input: row r <-> frame row yin + r, column c <-> x = xa + c
+        constexpr int NIN = V2_BROWS + 2 * R;
+        const int xa = xv0 & ~15, yin = y0 - 2 - R;
+        const int ylo = max(0, g.g0), yhi = min(FH, g.g0 + g.H) - 1;  // frame rows present in the buffer
+        if (use_tma) {
+            tma_stage<R>(S, tmap, xv0, y0, g);
+            if (!interior) {  // the box read zeros outside the buffer: replicate the edges
+                __syncthreads();
+                replicate_edges<NIN, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
+                                                 max(0, ylo - yin), min(NIN - 1, yhi - yin));
+            }
+        } else {
+            // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
+            // clamped bytes where a word crosses the frame edge
+            constexpr int QW = V2_IN_COLS / 4;
+            const bool al4 = (reinterpret_cast<uintptr_t>(img) & 3) == 0;
+            for (int i = threadIdx.x; i < NIN * QW; i += V2_THREADS) {
+                const int r = i / QW, c = 4 * (i - r * QW);
+                const uint8_t* row = img + (size_t)(min(max(yin + r, ylo), yhi) - g.g0) * W;
+                const int X = xa + c;
+                uint32_t v;
+                if (al4 && X >= 0 && X + 3 < W) {
+                    v = __ldg(reinterpret_cast<const unsigned int*>(row + X));
+                } else {
+                    v = 0;
+                    for (int k = 0; k < 4; ++k) v |= (uint32_t)row[min(max(X + k, 0), W - 1)] << (8 * k);
+                }
+                *reinterpret_cast<uint32_t*>(&S.in[r][c]) = v;
+            }
             __syncthreads();
         }
     }
+    v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
+    __syncthreads();
+    if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
+        replicate_edges<V2_BROWS, V2_COLS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+                                           max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
+    v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
+    __syncthreads();
+    if (!interior)  // magnitudes: row j <-> frame row y0-1+j
+        replicate_edges<V3_MROWS, V2_COLS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+                                           max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R>(CP, xv0, y0, S, warp, lane, O);
 }
