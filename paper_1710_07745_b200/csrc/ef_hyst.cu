@@ -484,7 +484,10 @@ hyst_dense_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
 // pixels go to hyst_dense_kernel.
 // ---------------------------------------------------------------------------
 constexpr int WCAP = 512;
-constexpr int WT_WARPS = 4;  // tiles per block (small: a block holds its slot until its slowest tile ends)
+#ifndef EF_H1_WARPS
+#define EF_H1_WARPS 4
+#endif
+constexpr int WT_WARPS = EF_H1_WARPS;  // tiles per block (small: a block holds its slot until its slowest tile ends)
 
 struct WarpTile {
     unsigned long long fgrow[HT];
