@@ -82,47 +82,10 @@ __device__ __forceinline__ float u8f(uint32_t w, int k) {
     return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | (unsigned)k)) - 8388608.0f;
 }
 
-// Lanes whose 4 columns straddle the frame edge gather clamped bytes; kept
-// out of line so the interior path is a single 4-byte load.
-__device__ __noinline__ uint32_t load4_edge(const uint8_t* rowp, int c, int W) {
-    uint32_t w = 0;
-    for (int k = 0; k < 4; ++k) w |= (uint32_t)rowp[clampi(c + k, 0, W - 1)] << (8 * k);
-    return w;
-}
-
-__device__ __forceinline__ uint32_t load4(const uint8_t* rowp, int c, int W, bool col_ok) {
-    if (col_ok) return __ldg(reinterpret_cast<const unsigned int*>(rowp + c));
-    return load4_edge(rowp, c, W);
-}
-
 __device__ __forceinline__ float sqrt_apx(float x) {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-
-// Replace values at out-of-frame columns by the edge column's value.
-__device__ __forceinline__ void edge_fix(float (&v)[4], int xv0, int lane, int W) {
-    const int c = xv0 + 4 * lane;
-    if (xv0 < 0) {
-        const int L0 = (-xv0) >> 2, k0 = (-xv0) & 3;
-        float e0 = __shfl_sync(0xffffffffu, v[0], L0), e1 = __shfl_sync(0xffffffffu, v[1], L0);
-        float e2 = __shfl_sync(0xffffffffu, v[2], L0), e3 = __shfl_sync(0xffffffffu, v[3], L0);
-        float e = k0 == 0 ? e0 : (k0 == 1 ? e1 : (k0 == 2 ? e2 : e3));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (c + k < 0) v[k] = e;
-    }
-    if (xv0 + V2_COLS > W) {
-        const int last = W - 1 - xv0;
-        const int L1 = last >> 2, k1 = last & 3;
-        float e0 = __shfl_sync(0xffffffffu, v[0], L1), e1 = __shfl_sync(0xffffffffu, v[1], L1);
-        float e2 = __shfl_sync(0xffffffffu, v[2], L1), e3 = __shfl_sync(0xffffffffu, v[3], L1);
-        float e = k1 == 0 ? e0 : (k1 == 1 ? e1 : (k1 == 2 ? e2 : e3));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (c + k >= W) v[k] = e;
-    }
 }
 
 // ---------------------------------------------------------------- phase 1 --
@@ -131,33 +94,20 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
-// Rows of b computed per warp in phase 1: the tile's 68 b rows split 4 ways.
-constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 17
+// Rows of b computed per warp in phase 1: the tile's 36 b rows split 4 ways.
+constexpr int V2_P1_ROWS = (V2_BROWS + V2_WARPS - 1) / V2_WARPS;  // 9
+static_assert(V2_P1_ROWS * V2_WARPS == V2_BROWS, "phase 1 rows split evenly");
 
-template <int R, bool INTERIOR, bool STAGED, class Smem>
-__device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const FrameGeom& g, int xv0, int y0,
-                                          const FastParams& P, Smem& S, int warp, int lane) {
+// Phase 1 over the staged input tile (all rows and columns present: edge
+// tiles have replicated their margins).  Warp w computes blurred rows
+// ys .. ys + V2_P1_ROWS - 1 (frame rows), ys = y0 - 2 + w * V2_P1_ROWS.
+template <int R, class Smem>
+__device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, Smem& S, int warp, int lane) {
     constexpr int NR = V2Cfg<R>::NR;
-    const int c = xv0 + 4 * lane;
-    const int W = g.W;
-    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
-    const bool col_ok = INTERIOR || (c >= 0 && c + 3 < W);
-    // b rows of this warp: global ys .. ys+16 (a fixed trip count keeps the
-    // warp converged; rows outside the frame are computed from clamped input
-    // and simply not stored)
     const int ys = y0 - 2 + warp * V2_P1_ROWS;
-    const int vlo = max(ys, max(y0 - 2, 0));
-    const int vhi = min(ys + V2_P1_ROWS, min(y0 + V2_TH + 2, g.full_H));
-    // input rows clamp to the frame and to the rows present in the buffer
-    const int rlo = max(0, g.g0), rhi = min(g.full_H - 1, g.g0 + g.H - 1);
-    const uint8_t* base = img - (ptrdiff_t)g.g0 * W;
-    // interior tiles never clamp (all input rows exist); 32-bit row offsets
-    auto rowp = [&](int Y) { return base + (INTERIOR ? Y : min(max(Y, rlo), rhi)) * W; };
-    // STAGED: the whole input tile (rows y0-2-R ..) is in shared memory already
-    auto in_row = [&](int Y) -> uint32_t {
+    auto fetch = [&](int Y) -> uint32_t {  // 4 staged input bytes of frame row Y
         return *reinterpret_cast<const uint32_t*>(&S.in[Y - (y0 - 2 - R)][(xv0 & 15) + 4 * lane]);
     };
-    auto fetch = [&](int Y) -> uint32_t { return STAGED ? in_row(Y) : load4(rowp(Y), c, W, col_ok); };
     float2 wf2[R + 1];
 #pragma unroll
     for (int k = 0; k <= R; ++k) wf2[k] = f2(P.wf[k], P.wf[k]);
@@ -227,13 +177,7 @@ __device__ __forceinline__ void v2_phase1(const uint8_t* __restrict__ img, const
                 b23.y = fmaf(wf2[o].x, e[11 - o] + e[11 + o], b23.y);
             }
         }
-        float b[4] = {b01.x, b01.y, b23.x, b23.y};
-        if (edge) edge_fix(b, xv0, lane, W);
-        const int Y = ys + u;
-        if (INTERIOR || (Y >= vlo && Y < vhi)) {
-            *reinterpret_cast<float2*>(out) = f2(b[0], b[1]);
-            *reinterpret_cast<float2*>(out + 2) = f2(b[2], b[3]);
-        }
+        *reinterpret_cast<float4*>(out) = make_float4(b01.x, b01.y, b23.x, b23.y);
         out += V2_COLS;
     }
 }
@@ -402,7 +346,7 @@ __device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], floa
     sm[3] = fmaf(2.f, bb.w, bb.z + br);
 }
 
-template <int R, bool INTERIOR>
+template <int R>
 __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, const FastParams& P, V3Smem& S,
                                            int warp, int lane, const V2Out& O) {
     constexpr int HXA = V2Cfg<R>::HXA;
@@ -413,18 +357,14 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     // loop exit around the shuffles and votes); rows 25 and 26 are computed
     // twice, with identical values, labels and candidate words.
     const int j0 = min(warp * V3_MPW, V3_MROWS - V3_MPW);
-    const int oy0 = g.out0, oy1 = g.out0 + g.rows;
-    const int ylim = min(oy1, FH);  // rows at or past this are not classified here
-    const bool edge = !INTERIOR && (xv0 < 0 || xv0 + V2_COLS > W);
+    const int ylim = min(g.out0 + g.rows, FH);  // rows at or past this are not classified here
     const int c = xv0 + 4 * lane;
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
     const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
     const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
     const int l = 4 * lane;
     const int Wq = W >> 2;
-    auto brow = [&](int Y) -> const float* {
-        return &S.b[(INTERIOR ? Y : clampi(Y, 0, FH - 1)) - (y0 - 2)][l];
-    };
+    auto brow = [&](int Y) -> const float* { return &S.b[Y - (y0 - 2)][l]; };
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
     const long long fin_off = S.bits.fg ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
     float d[3][4], sm[3][4];
@@ -443,19 +383,13 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const float2 gy23 = add2(f2(sm[pd][2], sm[pd][3]), f2(-sm[pu][2], -sm[pu][3]));
         float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
         float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
-        if (edge) {
-            float m4[4] = {m01.x, m01.y, m23.x, m23.y};
-            edge_fix(m4, xv0, lane, W);
-            m01 = f2(m4[0], m4[1]);
-            m23 = f2(m4[2], m4[3]);
-        }
         *reinterpret_cast<float4*>(&S.m[j][l]) = make_float4(m01.x, m01.y, m23.x, m23.y);
         // output rows: groups certainly below `low` get the background class
         // now, the others are marked for the classifier
         // (straight-line: the vote runs on every row, the stores are predicated,
         // so no divergent region surrounds the vote)
         const bool outrow = j >= 1 && j <= V2_TH;
-        const bool act = outrow && out_lane && Ym < ylim && (INTERIOR || Ym >= oy0);
+        const bool act = outrow && out_lane && Ym < ylim;
         const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
         const unsigned b0 = __ballot_sync(0xffffffffu, cand);
         if (act && !cand) {
@@ -604,12 +538,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             __syncthreads();
         }
     }
-    v2_phase1<R, true, true>(img, g, xv0, y0, P, S, warp, lane);
+    v2_phase1<R>(xv0, y0, P, S, warp, lane);
     __syncthreads();
     if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
         replicate_edges<V2_BROWS, V2_COLS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
-    v3_phase2a<R, true>(g, xv0, y0, P, S, warp, lane, O);
+    v3_phase2a<R>(g, xv0, y0, P, S, warp, lane, O);
     __syncthreads();
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
