@@ -144,7 +144,7 @@ ex_tile_kernel(const In* __restrict__ src, int H, int W, ExactParams P, uint8_t*
 constexpr int FX_WARPS = 4;
 
 __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom& g, int y, int x,
-                               const ExactParams& P, double* s_h, double* s_b, uint8_t* out,
+                               const ExactParams& P, double* s_h, double* s_b, double* s_m, uint8_t* out,
                                unsigned long long* ambiguous) {
     const int lane = threadIdx.x & 31;
     const int r = P.r, H = g.full_H, W = g.W;
@@ -173,26 +173,35 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
         }
     }
     __syncwarp();
-    if (lane == 0) {
-        auto Bv = [&](int Y, int X) {
-            return s_b[(clampi(Y, 0, H - 1) - (y - 2)) * 5 + (clampi(X, 0, W - 1) - (x - 2))];
-        };
-        auto grad = [&](int Y, int X, double& gx, double& gy) {
-            double blk[3][3];
-            for (int dy = 0; dy < 3; ++dy)
-                for (int dx = 0; dx < 3; ++dx) blk[dy][dx] = Bv(Y + dy - 1, X + dx - 1);
-            exact_sobel(blk, gx, gy);
-        };
+    auto Bv = [&](int Y, int X) {
+        return s_b[(clampi(Y, 0, H - 1) - (y - 2)) * 5 + (clampi(X, 0, W - 1) - (x - 2))];
+    };
+    auto grad = [&](int Y, int X, double& gx, double& gy) {
+        double blk[3][3];
+        for (int dy = 0; dy < 3; ++dy)
+            for (int dx = 0; dx < 3; ++dx) blk[dy][dx] = Bv(Y + dy - 1, X + dx - 1);
+        exact_sobel(blk, gx, gy);
+    };
+    // lanes 0..8: gradient magnitude at the 3x3 positions around the pixel
+    // (clamped), in parallel -- the NMS needs the centre and two of them
+    if (lane < 9) {
+        const int dy = lane / 3 - 1, dx = lane % 3 - 1;
         double gx, gy;
-        grad(y, x, gx, gy);
-        double c = exact_mag(gx, gy);
-        int s = exact_sector(gx, gy, ambiguous);
+        grad(clampi(y + dy, 0, H - 1), clampi(x + dx, 0, W - 1), gx, gy);
+        s_m[lane] = exact_mag(gx, gy);
+        if (lane == 4) {
+            s_m[9] = gx;
+            s_m[10] = gy;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const double c = s_m[4];
+        const int s = exact_sector(s_m[9], s_m[10], ambiguous);
         int dy1, dx1, dy2, dx2;
         nb_offsets(s, dy1, dx1, dy2, dx2);
-        double g1x, g1y, g2x, g2y;
-        grad(clampi(y + dy1, 0, H - 1), clampi(x + dx1, 0, W - 1), g1x, g1y);
-        grad(clampi(y + dy2, 0, H - 1), clampi(x + dx2, 0, W - 1), g2x, g2y);
-        double t = (c >= exact_mag(g1x, g1y) && c >= exact_mag(g2x, g2y)) ? c : 0.0;
+        const double m1 = s_m[(dy1 + 1) * 3 + (dx1 + 1)], m2 = s_m[(dy2 + 1) * 3 + (dx2 + 1)];
+        const double t = (c >= m1 && c >= m2) ? c : 0.0;
         *out = classify_exact(t, P.low, P.high);  // nms.py:51-52, hysteresis.py:57-59
     }
     __syncwarp();
@@ -225,6 +234,7 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
                 const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
+    __shared__ double s_m[FX_WARPS][11];
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5;
@@ -235,7 +245,7 @@ fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uin
         unsigned long long idx = list[e], f;
         int y, x;
         out_coords(idx, g, f, y, x);
-        fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
+        fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
                        labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
         fix_bits(B, g, f, y, x, labels[idx], labels + idx);
     }
@@ -248,6 +258,7 @@ fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, Exa
                 uint8_t* labels, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
+    __shared__ double s_m[FX_WARPS][11];
     pdl_wait();
     pdl_trigger();
     if (!hdr->overflow) return;
@@ -264,7 +275,7 @@ fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, Exa
             unsigned long long p = base + l, f;
             int y, x;
             out_coords(p, g, f, y, x);
-            fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp],
+            fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
                            labels + p, (unsigned long long*)&hdr->stats.ambiguous);
             fix_bits(B, g, f, y, x, labels[p], labels + p);
         }
