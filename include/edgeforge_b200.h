@@ -141,6 +141,13 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
                      const double* h_weights, int32_t radius, double low, double high,
                      uint8_t* h_labels, uint8_t* h_final, int32_t device);
 
+/* Host helper for the drop-in's integer test (GrayImage holds float64,
+ * image.py:23-50; the u8 fast path applies when every pixel is an integer in
+ * [0,255]): converts n float64 pixels to u8 with the host thread pool.
+ * Returns 1 when every value was such an integer (dst complete), 0 when not
+ * (dst unspecified), EF_EINVAL on bad arguments.  No device involved. */
+int ef_host_f64_to_u8(const double* src, int64_t n, uint8_t* dst);
+
 /* ---- Row-band partition of one huge frame (multi-GPU, trace_edges_parallel
  * hysteresis.py:90-131 generalised across devices). -----------------------
  *

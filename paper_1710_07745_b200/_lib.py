@@ -39,6 +39,7 @@ _SIGNATURES = {
     "ef_reset_stats": ([P, SZ, P], ctypes.c_int),
     "ef_read_stats": ([P, SZ, P, ctypes.POINTER(EfStats)], ctypes.c_int),
     "ef_set_classify_events": ([P, P], ctypes.c_int),
+    "ef_host_f64_to_u8": ([P, I64, P], ctypes.c_int),
     "ef_canny_u8": ([P, I64, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
     "ef_canny_f64": ([P, I64, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
     "ef_classify_u8": ([P, I64, I32, I32, P, I32, D, D, P, P, SZ, P], ctypes.c_int),

@@ -649,6 +649,11 @@ std::vector<int64_t> chunk_plan(int64_t batch, size_t fpx) {
 }
 }  // namespace
 
+int ef_host_f64_to_u8(const double* src, int64_t n, uint8_t* dst) {
+    if (n < 0 || (n > 0 && (!src || !dst))) return fail(EF_EINVAL, "bad buffers");
+    return parallel_f64_to_u8(src, (size_t)n, dst) ? 1 : 0;
+}
+
 int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_t width, const double* h_weights,
                      int32_t radius, double low, double high, uint8_t* h_labels, uint8_t* h_final,
                      int32_t device) {

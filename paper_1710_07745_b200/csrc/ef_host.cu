@@ -17,6 +17,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -261,6 +262,40 @@ static void stream_copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
     }
     _mm_sfence();
     for (; i < bytes; ++i) dst[i] = src[i];
+}
+
+static bool f64_to_u8(const double* src, size_t n, uint8_t* dst) {
+    bool ok = true;
+    for (size_t i = 0; i < n; ++i) {
+        const double v = src[i];
+        const bool in = v >= 0.0 && v <= 255.0;  // false for NaN
+        const int t = in ? (int)v : 0;
+        ok &= in && (double)t == v;
+        dst[i] = (uint8_t)t;
+    }
+    return ok;
+}
+
+bool parallel_f64_to_u8(const double* src, size_t n, uint8_t* dst) {
+    HostPool& P = host_pool();
+    const size_t parts = std::min<size_t>((size_t)P.size(), std::max<size_t>(1, n >> 18));
+    if (parts <= 1) return f64_to_u8(src, n, dst);
+    const size_t per = (n / parts + 4095) & ~size_t(4095);
+    Latch L;
+    std::atomic<bool> all_ok{true};
+    std::vector<std::pair<size_t, size_t>> ranges;
+    for (size_t s = 0; s < n; s += per) ranges.emplace_back(s, std::min(n, s + per));
+    L.add((int)ranges.size() - 1);
+    for (size_t i = 1; i < ranges.size(); ++i) {
+        const auto r = ranges[i];
+        P.submit([=, &L, &all_ok] {
+            if (!f64_to_u8(src + r.first, r.second - r.first, dst + r.first)) all_ok = false;
+            L.done();
+        }, true);
+    }
+    if (!f64_to_u8(src + ranges[0].first, ranges[0].second - ranges[0].first, dst + ranges[0].first)) all_ok = false;
+    L.wait();
+    return all_ok;
 }
 
 void parallel_copy(uint8_t* dst, const uint8_t* src, size_t bytes) {

@@ -46,4 +46,7 @@ struct Latch {
 // memcpy split over the pool (used to stage pageable inputs into pinned memory)
 void parallel_copy(uint8_t* dst, const uint8_t* src, size_t bytes);
 
+// float64 -> u8 over the pool; true when every value is an integer in [0, 255]
+bool parallel_f64_to_u8(const double* src, size_t n, uint8_t* dst);
+
 }  // namespace ef

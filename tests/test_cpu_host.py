@@ -175,3 +175,18 @@ def test_unpack_codes_matches_scalar_decode(tmp_path):
     subprocess.run(["g++", "-O2", "-o", str(exe), src, lib, f"-Wl,-rpath,{os.path.dirname(lib)}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "unpack ok" in out
+
+
+def test_host_f64_to_u8_integer_test():
+    """GrayImage.as_u8 (the drop-in's fast-path test) through the library's
+    threaded float64 -> u8 pass: integers in [0,255] convert, anything else
+    (fractions, out of range, negatives) routes to the float64 path."""
+    rng = np.random.default_rng(7)
+    a = rng.integers(0, 256, size=(517, 1031)).astype(np.float64)
+    u8 = ef.GrayImage.from_array(a).as_u8()
+    assert u8 is not None and u8.dtype == np.uint8 and np.array_equal(u8, a)
+    for bad in (0.5, 255.5, 256.0, -1.0, 1e9):
+        b = a.copy()
+        b[rng.integers(0, 517), rng.integers(0, 1031)] = bad
+        assert ef.GrayImage.from_array(b).as_u8() is None, bad
+    assert ef.GrayImage.from_array(np.zeros((3, 5))).as_u8() is not None
