@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -224,6 +225,9 @@ HostPool& host_pool() {
         cpu_set_t set;
         int n = 8;
         if (sched_getaffinity(0, sizeof set, &set) == 0) n = CPU_COUNT(&set);
+        // one process per GPU (torchrun): share the host's cores between the
+        // local ranks instead of oversubscribing them
+        if (const char* lw = getenv("LOCAL_WORLD_SIZE")) n = std::max(1, n / std::max(1, atoi(lw)));
         return new HostPool(std::max(1, std::min(n, 32)));
     }();
     return *pool;
