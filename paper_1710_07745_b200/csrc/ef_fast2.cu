@@ -311,11 +311,7 @@ __device__ __forceinline__ void tma_stage(Smem& S, const CUtensorMap& tmap, int 
 // ---------------------------------------------------------------------------
 constexpr int V3_MROWS = V2_TH + 2;                                   // magnitude rows y0-1 .. y0+TH
 constexpr int V3_MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;          // 9 per warp
-#ifndef EF_K1_QCAP
-#define EF_K1_QCAP 64
-#endif
-constexpr int V3_QCAP = EF_K1_QCAP;  // >= 32; a word that would overflow waits for a flush
-static_assert(V3_QCAP >= 32 && V3_QCAP <= 64, "queue capacity");
+
 
 struct V3Smem {
     float b[V2_BROWS][V2_COLS];
@@ -324,7 +320,6 @@ struct V3Smem {
         unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
     };
     unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
-    unsigned short q[V2_WARPS][V3_QCAP];            // per-warp compaction queue: row << 7 | column
     unsigned long long mbar;
     FgBits bits;
 };
@@ -412,47 +407,54 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     }
 }
 
+// position of the n-th (0-based) set bit of w
+__device__ __forceinline__ int select32(unsigned w, int n) {
+    int pos = 0;
+    int c = __popc(w & 0xffffu);
+    if (n >= c) { n -= c; w >>= 16; pos += 16; }
+    c = __popc(w & 0xffu);
+    if (n >= c) { n -= c; w >>= 8; pos += 8; }
+    c = __popc(w & 0xfu);
+    if (n >= c) { n -= c; w >>= 4; pos += 4; }
+    c = __popc(w & 0x3u);
+    if (n >= c) { n -= c; w >>= 2; pos += 2; }
+    return pos + (n >= (int)(w & 1u) ? 1 : 0);
+}
+
+// Phase 3: this warp's candidate words (rows warp + 4 i) sit one per lane; a
+// warp prefix count numbers their groups, and lane k takes group base + k --
+// found by a binary search over the prefix counts and a bit select -- so every
+// round classifies 32 groups with no queue in shared memory.
 template <int R>
 __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
                                          const V2Out O) {
-    const int FH = P.FH;
-    // this warp's 8 candidate words (rows warp + 4 i), one per lane; only
-    // non-empty words are visited
+    constexpr int NW = (V2_TH + V2_WARPS - 1) / V2_WARPS;  // candidate words per warp
+    static_assert(NW <= 32, "one word per lane");
     const int wrow = warp + V2_WARPS * lane;
-    const unsigned word = (lane < (V2_TH + V2_WARPS - 1) / V2_WARPS && wrow < V2_TH) ? S.cmask[wrow] : 0u;
-    unsigned nz = __ballot_sync(0xffffffffu, word != 0u);
-    int qn = 0;
-    while (nz || qn) {
-        if (nz) {  // append one word's groups if they fit, else classify first
-            const int i = __ffs(nz) - 1;
-            const unsigned mask = __shfl_sync(0xffffffffu, word, i);
-            if (qn + __popc(mask) <= V3_QCAP) {
-                nz &= nz - 1;
-                const int r = warp + V2_WARPS * i;
-                if ((mask >> lane) & 1u)
-                    S.q[warp][qn + __popc(mask & ((1u << lane) - 1u))] = (unsigned short)((r << 7) | lane);
-                qn += __popc(mask);
-                if (qn < 32 && nz) continue;
-            }
+    const unsigned word = (lane < NW && wrow < V2_TH) ? S.cmask[wrow] : 0u;
+    int incl = __popc(word);  // inclusive prefix over the lanes (lanes >= NW add 0)
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    constexpr int NW2 = NW <= 1 ? 1 : (NW <= 2 ? 2 : (NW <= 4 ? 4 : (NW <= 8 ? 8 : (NW <= 16 ? 16 : 32))));
+    for (int base = 0; base < total; base += 32) {
+        const int k = base + lane;
+        int i = 0;  // first word whose inclusive count exceeds k
+#pragma unroll
+        for (int step = NW2 / 2; step >= 1; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, i + step - 1);
+            if (v <= k) i += step;
         }
-        // classify 32 (or the last few) with every lane busy
-        __syncwarp();
-        const int take = min(qn, 32);
-        if (lane < take) {
-            const int e = S.q[warp][lane];
-            const int j = e >> 7, Yc = y0 + j;  // m tile row of Yc is j + 1
-            const float* bu = S.b[clampi(Yc - 1, 0, FH - 1) - (y0 - 2)];
-            const float* bd = S.b[clampi(Yc + 1, 0, FH - 1) - (y0 - 2)];
-            classify_group_bf(P, xv0, Yc, e & 127, S.m[j], S.m[j + 1], S.m[j + 2], bu, S.b[Yc - (y0 - 2)], bd,
-                              S.bits, O);
+        const unsigned w = __shfl_sync(0xffffffffu, word, i);
+        const int before = __shfl_sync(0xffffffffu, incl, i) - __popc(w);
+        if (k < total) {
+            const int j = warp + V2_WARPS * i;  // output row y0 + j; m tile rows j..j+2, b rows j+1..j+3
+            classify_group_bf(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
+                              S.b[j + 2], S.b[j + 3], S.bits, O);
         }
-        __syncwarp();
-        const int rest = qn - take;
-        const unsigned short moved = lane < rest ? S.q[warp][32 + lane] : 0;
-        __syncwarp();
-        if (lane < rest) S.q[warp][lane] = moved;
-        qn = rest;
-        __syncwarp();
     }
 }
 
