@@ -205,6 +205,7 @@ __device__ __forceinline__ void load6(const float* row, int cc0, float (&v)[6]) 
     v[5] = row[cc0 + 4];
 }
 
+template <bool FUSED>
 __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
                                                   const float* mc, const float* md, const float* bu,
                                                   const float* bm, const float* bd, const FgBits& bits,
@@ -256,7 +257,7 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
         }
     }
     *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
-    if (bits.fg) {
+    if (FUSED) {
         // final = strong (kFlag bytes give 0: the fix-up writes them)
         *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0 + bits.fin_off) = (packed >> 1) & 0x01010101u;
         // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
@@ -341,7 +342,7 @@ __device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], floa
     sm[3] = fmaf(2.f, bb.w, bb.z + br);
 }
 
-template <int R>
+template <int R, bool FUSED>
 __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, const FastParams& P, V3Smem& S,
                                            int warp, int lane, const V2Out& O) {
     constexpr int HXA = V2Cfg<R>::HXA;
@@ -361,7 +362,8 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     const int Wq = W >> 2;
     auto brow = [&](int Y) -> const float* { return &S.b[Y - (y0 - 2)][l]; };
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
-    const long long fin_off = S.bits.fg ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
+    const long long fin_off = FUSED ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
+    unsigned* const cmask = S.cmask;
     float d[3][4], sm[3][4];
     sobel_row(brow(y0 - 2 + j0), d[0], sm[0]);
     sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
@@ -387,11 +389,10 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const bool act = outrow && out_lane && Ym < ylim;
         const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
         const unsigned b0 = __ballot_sync(0xffffffffu, cand);
-        if (act && !cand) {
-            *lab = fill;
-            if (fin_off) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
-        }
-        if (lane == 0 && outrow) S.cmask[j - 1] = b0;
+        const bool bg = act && !cand;
+        if (bg) *lab = fill;
+        if (FUSED && bg) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
+        if (lane == 0 && outrow) cmask[j - 1] = b0;
         lab += Wq;
     };
     if constexpr (V3_MPW % 3 == 0) {
@@ -425,7 +426,7 @@ __device__ __forceinline__ int select32(unsigned w, int n) {
 // warp prefix count numbers their groups, and lane k takes group base + k --
 // found by a binary search over the prefix counts and a bit select -- so every
 // round classifies 32 groups with no queue in shared memory.
-template <int R>
+template <int R, bool FUSED>
 __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
                                          const V2Out O) {
     constexpr int NW = (V2_TH + V2_WARPS - 1) / V2_WARPS;  // candidate words per warp
@@ -452,7 +453,7 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
         const int before = __shfl_sync(0xffffffffu, incl, i) - __popc(w);
         if (k < total) {
             const int j = warp + V2_WARPS * i;  // output row y0 + j; m tile rows j..j+2, b rows j+1..j+3
-            classify_group_bf(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
+            classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
                               S.b[j + 2], S.b[j + 3], S.bits, O);
         }
     }
@@ -485,7 +486,7 @@ __device__ __forceinline__ void replicate_edges(T (*a)[NCOLS], int c_lo, int c_h
     }
 }
 
-template <int R>
+template <int R, bool FUSED>
 __global__ void __launch_bounds__(V2_THREADS, EF_K1_MINB)
 k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
             unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
@@ -545,13 +546,13 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
         replicate_edges<V2_BROWS, V2_COLS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
-    v3_phase2a<R>(g, xv0, y0, P, S, warp, lane, O);
+    v3_phase2a<R, FUSED>(g, xv0, y0, P, S, warp, lane, O);
     __syncthreads();
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
-    v3_classify<R>(CP, xv0, y0, S, warp, lane, O);
+    v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
 
 bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 6 && (g.W % 4) == 0; }
@@ -589,15 +590,20 @@ template <int R>
 static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                             uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
                             cudaStream_t st) {
-    auto kern = k1v3_kernel<R>;
+    // FUSED (bit planes + final map) is a compile-time variant: the per-row
+    // checks would otherwise sit in the hottest loop
+    auto kern = B.fg ? k1v3_kernel<R, true> : k1v3_kernel<R, false>;
     const int smem = (int)sizeof(V3Smem);
     static std::atomic<uint64_t> configured{0};
     cudaError_t e = once_per_device(configured, [&] {
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        // occupancy is shared-memory bound: ask for the largest carveout
-        if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     (int)cudaSharedmemCarveoutMaxShared);
+        cudaError_t r = cudaSuccess;
+        for (auto k : {k1v3_kernel<R, true>, k1v3_kernel<R, false>}) {
+            if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            // occupancy is shared-memory bound: ask for the largest carveout
+            if (r == cudaSuccess)
+                r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared);
+        }
         return r;
     });
     if (e != cudaSuccess) return e;
