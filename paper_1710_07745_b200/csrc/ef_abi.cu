@@ -282,6 +282,7 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
         // the certified bounds assume a convex (non-negative) kernel; a signed
         // kernel takes the exact float64 kernel instead
         if (g.g0 != 0 || g.full_H != g.H || g.rows != g.H) return fail(EF_EINVAL, "signed kernel on a band");
+        EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");  // the trace that follows reuses the counters
         ExactParams XP = make_exact(w, r, low, high);
         EF_CHECK(launch_exact<uint8_t>(src, batch, g.H, g.W, XP, labels, nullptr, nullptr, nullptr, nullptr,
                                        nullptr, nullptr, nullptr, ws.hdr, st),
@@ -294,9 +295,9 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     static const bool no_bits = getenv("EF_NO_FG_BITS") != nullptr;  // A/B switch for profiling
     if (fin && bits && !no_bits && k1_emits_bits(FP, g)) {
         const int words = (g.W + 63) / 64;
+        nwords = (unsigned long long)(ws.stbits - ws.fgbits) + (unsigned long long)batch * g.rows * words;
         B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)g.rows * words,
                    (long long)(reinterpret_cast<intptr_t>(fin) - reinterpret_cast<intptr_t>(labels))};
-        nwords = (unsigned long long)(ws.stbits - ws.fgbits) + (unsigned long long)batch * g.rows * words;
         *bits = B;
     }
     EF_CHECK(launch_ws_begin(ws, L, nwords, sms, st), "ws_begin");

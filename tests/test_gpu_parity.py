@@ -198,6 +198,20 @@ def test_node_list_overflow_large_noise(canny):
     assert np.array_equal(_np(fin).astype(bool), ef_)
 
 
+def test_signed_kernel_takes_exact_path(canny):
+    """A kernel with negative taps (GaussianKernel accepts any weights) is not
+    covered by the fp32 certification: the exact float64 kernel runs, followed by
+    the same hysteresis -- through the fused entry and through run_pipeline."""
+    rng = np.random.default_rng(21)
+    w = np.array([-0.05, 0.3, 0.5, 0.3, -0.05])
+    for _ in range(2):  # twice: the second call must not see the first one's counters
+        frames = synth.config1(2, 130, 200)
+        frames[1] = rng.integers(0, 256, size=frames.shape[1:], dtype=np.uint8)
+        el, ef_ = O.canny(frames, w, 20.0, 50.0)
+        lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+        assert np.array_equal(_np(lab), el) and np.array_equal(_np(fin).astype(bool), ef_)
+
+
 def test_float_path_random_vs_oracle(canny):
     rng = np.random.default_rng(5)
     for (h, wd) in [(1, 1), (7, 5), (33, 47), (128, 96)]:
