@@ -823,10 +823,43 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
     }
 }
 
+// H2 helpers.  A seam is a pair of 64-vectors held two per lane (v0: index
+// lane, v1: index lane + 32); neighbours at index +-1 come by shuffles.
+__device__ __forceinline__ void vec_neighbours(int v0, int v1, int lane, int& m0, int& p0, int& m1, int& p1) {
+    const int u0 = __shfl_up_sync(0xffffffffu, v0, 1), u1 = __shfl_up_sync(0xffffffffu, v1, 1);
+    const int d0 = __shfl_down_sync(0xffffffffu, v0, 1), d1 = __shfl_down_sync(0xffffffffu, v1, 1);
+    const int w1 = __shfl_sync(0xffffffffu, v1, 0), w0 = __shfl_sync(0xffffffffu, v0, 31);
+    m0 = lane == 0 ? -1 : u0;
+    m1 = lane == 0 ? w0 : u1;
+    p0 = lane == 31 ? w1 : d0;
+    p1 = lane == 31 ? -1 : d1;
+}
+
+// unions of A[i] with C[i-1], C[i], C[i+1] (entries < 0: no component).  A
+// run of equal A's along the seam unites each C once: the index before has
+// already united C[i-1] and C[i].
+__device__ __forceinline__ void seam_unite(int* gpar, int a0, int a1, int c0, int c1, int lane) {
+    int cm0, cp0, cm1, cp1, am0, ap0, am1, ap1;
+    vec_neighbours(c0, c1, lane, cm0, cp0, cm1, cp1);
+    vec_neighbours(a0, a1, lane, am0, ap0, am1, ap1);
+    auto one = [&](int a, int aprev, int cm, int c, int cp) {
+        if (a < 0) return;
+        const bool run = a == aprev;
+        if (!run && cm >= 0) gunite(gpar, a, cm);
+        if (!run && c >= 0 && c != cm) gunite(gpar, a, c);
+        if (cp >= 0 && cp != c && cp != cm) gunite(gpar, a, cp);
+    };
+    one(a0, am0, cm0, c0, cp0);
+    one(a1, am1, cm1, c1, cp1);
+}
+
 // H2: unions across tile seams, one warp per tile (8 per block; grid
-// (ceil(tiles per frame / 8), frames)): right seam rows, bottom seam columns,
-// and the two lower corner diagonals.  Tiles without perimeter components --
-// and seams whose other side has none -- are skipped on one byte.
+// (ceil(tiles per frame / 8), frames)): the right seam, the bottom seam and
+// the two lower corner diagonals.  Tiles without perimeter components -- and
+// seams whose other side has none -- are skipped on one byte.  Both seams'
+// loads are issued before any union (one round trip, not two), and runs of
+// one component along a seam unite once.  Perimeter slots outside the valid
+// extent hold -1.
 __global__ void __launch_bounds__(256)
 hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
     pdl_wait();
@@ -838,50 +871,30 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
     const long long tile = (long long)blockIdx.y * tpf + t;
     if (!b.border[tile]) return;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    const TileGeo g = tile_geo_xyz(tx, ty, blockIdx.y, H, W);
+    const bool right = tx + 1 < tiles_x, down = ty + 1 < tiles_y;
+    const bool mr = right && b.border[tile + 1];
+    const bool md = down && b.border[tile + tiles_x];
+    const bool mdr = right && down && b.border[tile + tiles_x + 1];
+    const bool mdl = tx > 0 && down && b.border[tile + tiles_x - 1];
     const int* pa = b.perim + tile * HP;
     int* gpar = b.gpar;
-    if (tx + 1 < tiles_x && b.border[tile + 1]) {
+    int ar0 = -1, ar1 = -1, cr0 = -1, cr1 = -1, ad0 = -1, ad1 = -1, cd0 = -1, cd1 = -1;
+    if (mr) {
         const int* pb = b.perim + (tile + 1) * HP;
-        for (int r = lane; r < g.vh; r += 32) {
-            const int a = pa[192 + r];
-            if (a < 0) continue;
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int y2 = r + dy;
-                if (y2 < 0 || y2 >= g.vh) continue;
-                const int c = pb[128 + y2];
-                if (c >= 0) gunite(gpar, a, c);
-            }
-        }
+        ar0 = pa[192 + lane]; ar1 = pa[192 + 32 + lane];  // my right column
+        cr0 = pb[128 + lane]; cr1 = pb[128 + 32 + lane];  // its left column
     }
-    if (ty + 1 < tiles_y) {
-        const TileGeo gc = tile_geo_xyz(tx, ty + 1, blockIdx.y, H, W);
-        if (b.border[tile + tiles_x]) {
-            const int* pc = b.perim + (tile + tiles_x) * HP;
-            for (int x = lane; x < g.vw; x += 32) {
-                const int a = pa[64 + x];
-                if (a < 0) continue;
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int x2 = x + dx;
-                    if (x2 < 0 || x2 >= gc.vw) continue;
-                    const int c = pc[x2];
-                    if (c >= 0) gunite(gpar, a, c);
-                }
-            }
-        }
-        if (lane == 0) {
-            if (tx + 1 < tiles_x && g.vw == HT && b.border[tile + tiles_x + 1]) {  // bottom-right -> (0,0) below-right
-                const int a = pa[64 + HT - 1];
-                const int d = b.perim[(tile + tiles_x + 1) * HP + 0];
-                if (a >= 0 && d >= 0) gunite(gpar, a, d);
-            }
-            if (tx > 0 && b.border[tile + tiles_x - 1]) {  // bottom-left -> (0, 63) below-left
-                const int a = pa[64 + 0];
-                const int d = b.perim[(tile + tiles_x - 1) * HP + HT - 1];
-                if (a >= 0 && d >= 0) gunite(gpar, a, d);
-            }
-        }
+    if (md) {
+        const int* pc = b.perim + (tile + tiles_x) * HP;
+        ad0 = pa[64 + lane]; ad1 = pa[64 + 32 + lane];  // my bottom row
+        cd0 = pc[lane]; cd1 = pc[32 + lane];            // its top row
     }
+    int ca = -1, cb = -1;  // corner pairs: lane 0 bottom-right, lane 1 bottom-left
+    if (lane == 0 && mdr) { ca = pa[64 + HT - 1]; cb = b.perim[(tile + tiles_x + 1) * HP + 0]; }
+    if (lane == 1 && mdl) { ca = pa[64 + 0]; cb = b.perim[(tile + tiles_x - 1) * HP + HT - 1]; }
+    if (mr) seam_unite(gpar, ar0, ar1, cr0, cr1, lane);
+    if (md) seam_unite(gpar, ad0, ad1, cd0, cd1, lane);
+    if (ca >= 0 && cb >= 0) gunite(gpar, ca, cb);
 }
 
 // H3: strong flag of every node onto its root, over the node-list stripes
