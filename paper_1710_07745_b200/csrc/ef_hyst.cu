@@ -869,31 +869,33 @@ hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
     const int t = blockIdx.x * 8 + warp;
     if (t >= tpf) return;
     const long long tile = (long long)blockIdx.y * tpf + t;
-    if (!b.border[tile]) return;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
     const bool right = tx + 1 < tiles_x, down = ty + 1 < tiles_y;
-    const bool mr = right && b.border[tile + 1];
-    const bool md = down && b.border[tile + tiles_x];
-    const bool mdr = right && down && b.border[tile + tiles_x + 1];
-    const bool mdl = tx > 0 && down && b.border[tile + tiles_x - 1];
+    // every load is issued before any is needed (the perimeters of tiles
+    // without border components are stale and ignored)
     const int* pa = b.perim + tile * HP;
+    const int* pb = b.perim + (right ? tile + 1 : tile) * HP;
+    const int* pc = b.perim + (down ? tile + tiles_x : tile) * HP;
+    const uint8_t bo = b.border[tile];
+    const uint8_t br = right ? b.border[tile + 1] : 0;
+    const uint8_t bd = down ? b.border[tile + tiles_x] : 0;
+    const int ar0 = pa[192 + lane], ar1 = pa[192 + 32 + lane];  // my right column
+    const int cr0 = pb[128 + lane], cr1 = pb[128 + 32 + lane];  // its left column
+    const int ad0 = pa[64 + lane], ad1 = pa[64 + 32 + lane];    // my bottom row
+    const int cd0 = pc[lane], cd1 = pc[32 + lane];              // its top row
+    if (!bo) return;
     int* gpar = b.gpar;
-    int ar0 = -1, ar1 = -1, cr0 = -1, cr1 = -1, ad0 = -1, ad1 = -1, cd0 = -1, cd1 = -1;
-    if (mr) {
-        const int* pb = b.perim + (tile + 1) * HP;
-        ar0 = pa[192 + lane]; ar1 = pa[192 + 32 + lane];  // my right column
-        cr0 = pb[128 + lane]; cr1 = pb[128 + 32 + lane];  // its left column
-    }
-    if (md) {
-        const int* pc = b.perim + (tile + tiles_x) * HP;
-        ad0 = pa[64 + lane]; ad1 = pa[64 + 32 + lane];  // my bottom row
-        cd0 = pc[lane]; cd1 = pc[32 + lane];            // its top row
-    }
     int ca = -1, cb = -1;  // corner pairs: lane 0 bottom-right, lane 1 bottom-left
-    if (lane == 0 && mdr) { ca = pa[64 + HT - 1]; cb = b.perim[(tile + tiles_x + 1) * HP + 0]; }
-    if (lane == 1 && mdl) { ca = pa[64 + 0]; cb = b.perim[(tile + tiles_x - 1) * HP + HT - 1]; }
-    if (mr) seam_unite(gpar, ar0, ar1, cr0, cr1, lane);
-    if (md) seam_unite(gpar, ad0, ad1, cd0, cd1, lane);
+    if (lane == 0 && right && down && b.border[tile + tiles_x + 1]) {
+        ca = pa[64 + HT - 1];
+        cb = b.perim[(tile + tiles_x + 1) * HP + 0];
+    }
+    if (lane == 1 && tx > 0 && down && b.border[tile + tiles_x - 1]) {
+        ca = pa[64 + 0];
+        cb = b.perim[(tile + tiles_x - 1) * HP + HT - 1];
+    }
+    if (br) seam_unite(gpar, ar0, ar1, cr0, cr1, lane);
+    if (bd) seam_unite(gpar, ad0, ad1, cd0, cd1, lane);
     if (ca >= 0 && cb >= 0) gunite(gpar, ca, cb);
 }
 
