@@ -670,17 +670,25 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
             s.info[e] = 0xffffu;
         }
         __syncwarp();
-        // unions with the row above
+        // unions with the row above, once per (run, run above) pair: a run's
+        // first pixel unites with the runs above touching x-1 .. x+1, every
+        // later pixel only with a run above that starts at x+1 (its left
+        // neighbour, same component, has covered x-2 .. x)
         for (int e = lane; e < n; e += 32) {
             const int pix = s.list[e];
             const int r = pix >> 6, x = pix & (HT - 1);
             if (r == 0) continue;
             const unsigned long long up = s.fgrow[r - 1];
-            if ((up >> x) & 1ull) {
+            const bool in_run = x > 0 && ((s.fgrow[r] >> (x - 1)) & 1ull);
+            const bool nx = (up >> x) & 1ull;
+            const bool nr = x < HT - 1 && ((up >> (x + 1)) & 1ull);
+            if (in_run) {
+                if (nr && !nx) sunite(s.par, e, cidx(s, r - 1, x + 1));
+            } else if (nx) {
                 sunite(s.par, e, cidx(s, r - 1, x));
             } else {
                 if (x > 0 && ((up >> (x - 1)) & 1ull)) sunite(s.par, e, cidx(s, r - 1, x - 1));
-                if (x < HT - 1 && ((up >> (x + 1)) & 1ull)) sunite(s.par, e, cidx(s, r - 1, x + 1));
+                if (nr) sunite(s.par, e, cidx(s, r - 1, x + 1));
             }
         }
         __syncwarp();
