@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 
@@ -88,11 +89,12 @@ __device__ __forceinline__ float sqrt_apx(float x) {
     return y;
 }
 
-// The blurred (b) and magnitude (m) tiles are stored with their 16-byte
-// column quads XOR-swizzled by row (quad q of row r at q ^ (r & 7)): rows are
-// 512 bytes apart, so without it the classifier's lanes -- 32 groups from
-// different rows, often one above the other along an edge -- hit the same banks.
-__device__ __forceinline__ int swz(int r, int q) { return 4 * (q ^ (r & 7)); }  // float offset of quad q in row r
+// The blurred (b) and magnitude (m) tiles have a padded row stride of 132
+// floats (528 bytes): quad q of row r starts in bank group (r + q) mod 8, so
+// the classifier's lanes -- 32 groups from different rows, often one above the
+// other along an edge -- do not collide on the banks of 512-byte rows.  (An
+// XOR swizzle does the same but costs address instructions in every phase.)
+constexpr int V2_CS = V2_COLS + 4;
 
 // ---------------------------------------------------------------- phase 1 --
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -183,7 +185,7 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
                 b23.y = fmaf(wf2[o].x, e[11 - o] + e[11 + o], b23.y);
             }
         }
-        *reinterpret_cast<float4*>(&S.b[rb + u][swz(rb + u, lane)]) = make_float4(b01.x, b01.y, b23.x, b23.y);
+        *reinterpret_cast<float4*>(&S.b[rb + u][4 * lane]) = make_float4(b01.x, b01.y, b23.x, b23.y);
     }
 }
 
@@ -203,30 +205,27 @@ struct V2Cls {
 // two scalar loads per row), and every pixel's class, sector and NMS decision
 // is computed with selects -- lanes of a warp classify different groups, so
 // branches would serialise every path.
-// (row r of a swizzled tile; quads cl - 1 .. cl + 1 exist: candidate groups
-// are never a lane's edge quad)
-__device__ __forceinline__ void load6(const float* row, int r, int cl, float (&v)[6]) {
-    const float4 mid = *reinterpret_cast<const float4*>(row + swz(r, cl));
-    v[0] = row[swz(r, cl - 1) + 3];
+__device__ __forceinline__ void load6(const float* row, int cc0, float (&v)[6]) {
+    const float4 mid = *reinterpret_cast<const float4*>(row + cc0);
+    v[0] = row[cc0 - 1];
     v[1] = mid.x; v[2] = mid.y; v[3] = mid.z; v[4] = mid.w;
-    v[5] = row[swz(r, cl + 1)];
+    v[5] = row[cc0 + 4];
 }
 
 template <bool FUSED>
-__device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Yc, int cl, int j, const float* mu,
+__device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
                                                   const float* mc, const float* md, const float* bu,
                                                   const float* bm, const float* bd, const FgBits& bits,
                                                   const V2Out& O) {
     const float t1 = 0.41421356237309503f;
     const int cc0 = 4 * cl;
     float Mu[6], Mc[6], Md[6], Bu[6], Bm[6], Bd[6];
-    // m tile rows j .. j+2, b tile rows j+1 .. j+3
-    load6(mu, j, cl, Mu);
-    load6(mc, j + 1, cl, Mc);
-    load6(md, j + 2, cl, Md);
-    load6(bu, j + 1, cl, Bu);
-    load6(bm, j + 2, cl, Bm);
-    load6(bd, j + 3, cl, Bd);
+    load6(mu, cc0, Mu);
+    load6(mc, cc0, Mc);
+    load6(md, cc0, Md);
+    load6(bu, cc0, Bu);
+    load6(bm, cc0, Bm);
+    load6(bd, cc0, Bd);
     uint32_t packed = 0;
     bool any_flag = false;
     const uint32_t cls0 = (uint32_t)P.cls0;
@@ -323,11 +322,12 @@ constexpr int V3_MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;          // 9 per w
 
 
 struct V3Smem {
-    float b[V2_BROWS][V2_COLS];
-    union {
-        float m[V3_MROWS][V2_COLS];                 // squared magnitudes
+    union {  // first: the TMA destination must be 128-byte aligned
+        float m[V3_MROWS][V2_CS];                   // squared magnitudes
         unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
     };
+static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, "TMA / float4 alignment");
+    float b[V2_BROWS][V2_CS];
     unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
     unsigned long long mbar;
     FgBits bits;
@@ -367,7 +367,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
     const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
     const int Wq = W >> 2;
-    auto brow = [&](int Y) -> const float* { return &S.b[Y - (y0 - 2)][swz(Y - (y0 - 2), lane)]; };
+    auto brow = [&](int Y) -> const float* { return &S.b[Y - (y0 - 2)][4 * lane]; };
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
     const long long fin_off = FUSED ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
     unsigned* const cmask = S.cmask;
@@ -387,7 +387,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const float2 gy23 = add2(f2(sm[pd][2], sm[pd][3]), f2(-sm[pu][2], -sm[pu][3]));
         float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
         float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
-        *reinterpret_cast<float4*>(&S.m[j][swz(j, lane)]) = make_float4(m01.x, m01.y, m23.x, m23.y);
+        *reinterpret_cast<float4*>(&S.m[j][4 * lane]) = make_float4(m01.x, m01.y, m23.x, m23.y);
         // output rows: groups certainly below `low` get the background class
         // now, the others are marked for the classifier
         // (straight-line: the vote runs on every row, the stores are predicated,
@@ -460,7 +460,7 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
         const int before = __shfl_sync(0xffffffffu, incl, i) - __popc(w);
         if (k < total) {
             const int j = warp + V2_WARPS * i;  // output row y0 + j; m tile rows j..j+2, b rows j+1..j+3
-            classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), j, S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
+            classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
                               S.b[j + 2], S.b[j + 3], S.bits, O);
         }
     }
@@ -471,10 +471,9 @@ __device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem&
 // in shared memory by replicating their edge rows / columns (np.pad edge at
 // every stage, the reference's border policy) -- after which the interior code
 // runs unchanged.  Columns first, then rows (corners = corner pixel).
-template <int NROWS, int NCOLS, bool SWZ, class T>
-__device__ __forceinline__ void replicate_edges(T (*a)[NCOLS], int c_lo, int c_hi, int r_lo, int r_hi) {
-    // element (r, c) of the tile (SWZ: quad-swizzled float tile, see swz)
-    auto at = [&](int r, int c) -> T& { return SWZ ? a[r][swz(r, c >> 2) + (c & 3)] : a[r][c]; };
+template <int NROWS, int NCOLS, int STRIDE, class T>
+__device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_hi, int r_lo, int r_hi) {
+    auto at = [&](int r, int c) -> T& { return a[r][c]; };  // (NCOLS logical columns of STRIDE)
     // only the out-of-frame margins are touched: one row per thread, then one
     // column per thread
     if (c_lo > 0 || c_hi < NCOLS - 1) {
@@ -526,7 +525,7 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             tma_stage<R>(S, tmap, xv0, y0, g);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
-                replicate_edges<NIN, V2_IN_COLS, false>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
+                replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
                                                  max(0, ylo - yin), min(NIN - 1, yhi - yin));
             }
         } else {
@@ -553,12 +552,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     v2_phase1<R>(xv0, y0, P, S, warp, lane);
     __syncthreads();
     if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
-        replicate_edges<V2_BROWS, V2_COLS, true>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+        replicate_edges<V2_BROWS, V2_COLS, V2_CS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
     v3_phase2a<R, FUSED>(g, xv0, y0, P, S, warp, lane, O);
     __syncthreads();
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
-        replicate_edges<V3_MROWS, V2_COLS, true>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
+        replicate_edges<V3_MROWS, V2_COLS, V2_CS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
