@@ -326,12 +326,13 @@ struct V3Smem {
         float m[V3_MROWS][V2_CS];                   // squared magnitudes
         unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
     };
-static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, "TMA / float4 alignment");
     float b[V2_BROWS][V2_CS];
     unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
     unsigned long long mbar;
     FgBits bits;
 };
+static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, "TMA / float4 alignment");
+
 
 // d = b[x+1] - b[x-1] and s = b[x-1] + 2 b[x] + b[x+1] for this lane's 4 columns
 __device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], float (&sm)[4]) {
