@@ -183,6 +183,16 @@ int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows,
 int ef_band_merge(int32_t nbands, int32_t width, const int64_t* h_ids, const uint8_t* h_strong,
                   uint8_t* h_strong_out);
 
+/* The same merge on the device, stream-ordered (no host round trip): every
+ * rank all_gathers the bands' ef_band_edges rows into one device array and
+ * runs this on it, reaching the identical decision.  Ids are band-LOCAL here
+ * (as ef_band_edges writes them; band k's block is made unique internally as
+ * k << 40 | id).  d_scratch: ef_band_merge_scratch_bytes(nbands, width) bytes.
+ * Output equals ef_band_merge on the globalised ids. */
+size_t ef_band_merge_scratch_bytes(int32_t nbands, int32_t width);
+int ef_band_merge_device(int32_t nbands, int32_t width, const int64_t* d_ids, const uint8_t* d_strong,
+                         uint8_t* d_strong_out, void* d_scratch, size_t scratch_bytes, void* stream);
+
 /* Apply the merged decision for this band's edge rows and finalise d_final. */
 int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width,
                      const uint8_t* d_labels, uint8_t* d_final, void* d_workspace,

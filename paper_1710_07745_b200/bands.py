@@ -12,8 +12,10 @@ components that reach a strong pixel.  Here:
   edge export    ef_band_edges: per column of the top and bottom row, the
                  band-local component root and whether it already holds a
                  strong pixel.  ids are made global as (band << 40) | root.
-  seam merge     ef_band_merge (host C union-find over at most 2*W*nbands
-                 entries -- tiny next to the image), identical on every rank.
+  seam merge     ef_band_merge_device (union-find over the nbands*2*W edge
+                 entries on the GPU, four stream-ordered launches), identical on
+                 every rank; ef_band_merge is the same merge on the host (used
+                 by backends without a device, and as the GPU tests' check).
   finalize       ef_band_finalize: mark merged-strong roots, re-finalise the
                  tiles that had undecided components.
 
@@ -21,7 +23,8 @@ Multi-GPU (one process per GPU, torch.distributed):
   halo exchange  each rank owns rows [row0, row0+rows) in HBM and needs
                  radius+2 rows from each neighbour: batch_isend_irecv over NCCL
                  (NVLink P2P); frame edges are clamped instead.
-  edge exchange  all_gather of the 2*W edge ids/flags (NCCL).
+  edge exchange  all_gather of the 2*W edge ids/flags (NCCL), device to
+                 device: no host round trip on the band path.
 The compute steps go through a backend object so that the orchestration runs
 under gloo on CPU in the tests with an oracle-backed backend.
 """
@@ -61,6 +64,28 @@ def merge_edges(ids_all: np.ndarray, strong_all: np.ndarray, width: int) -> np.n
     out = np.empty_like(strong)
     _lib.check(_lib.load().ef_band_merge(nb, width, ids.ctypes.data, strong.ctypes.data, out.ctypes.data),
                "ef_band_merge")
+    return out
+
+
+def merge_edges_device(ids_local, strong, width: int):
+    """Device seam merge (ef_band_merge_device).  ids_local/strong: (nbands,
+    2*width) int64/uint8 CUDA tensors, ids band-local as ef_band_edges writes
+    them.  Returns the merged strong flags, same shape, on the device."""
+    from . import canny
+
+    torch = canny.require_cuda()
+    nb = ids_local.shape[0]
+    ids_local = ids_local.contiguous()
+    strong = strong.contiguous()
+    lib = _lib.load()
+    need = lib.ef_band_merge_scratch_bytes(nb, width)
+    if need == 0:
+        raise ValueError(f"bad band merge dimensions: {nb} bands x {width}")
+    scratch = torch.empty(need, dtype=torch.uint8, device=ids_local.device)
+    out = torch.empty_like(strong)
+    st = int(torch.cuda.current_stream(ids_local.device).cuda_stream)
+    _lib.check(lib.ef_band_merge_device(nb, width, ids_local.data_ptr(), strong.data_ptr(), out.data_ptr(),
+                                        scratch.data_ptr(), need, st), "ef_band_merge_device")
     return out
 
 
@@ -108,6 +133,10 @@ class CudaBandBackend:
         _lib.check(rc, "ef_band_edges")
         return ids, strong
 
+    def merge(self, ids_all, strong_all):
+        """Seam merge of every band's gathered edge rows, on the device."""
+        return merge_edges_device(ids_all, strong_all, self.width)
+
     def finalize(self, strong_edges):
         rc = _lib.load().ef_band_finalize(strong_edges.data_ptr(), self.rows, self.width, self.labels.data_ptr(),
                                           self.final.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
@@ -117,7 +146,7 @@ class CudaBandBackend:
 
 
 def trace_bands_local(labels, plan: list[tuple[int, int]]):
-    """trace_edges_parallel on one GPU: band-local tracing + host seam merge."""
+    """trace_edges_parallel on one GPU: band-local tracing + device seam merge."""
     from . import canny
 
     torch = canny.require_cuda()
@@ -129,12 +158,11 @@ def trace_bands_local(labels, plan: list[tuple[int, int]]):
         be.trace(labels[s:e])
         ids, strong = be.edges()
         backends.append(be)
-        ids_all.append(globalize_ids(ids.cpu().numpy(), k))
-        strong_all.append(strong.cpu().numpy())
-    merged = merge_edges(np.stack(ids_all), np.stack(strong_all), w)
+        ids_all.append(ids)
+        strong_all.append(strong)
+    merged = merge_edges_device(torch.stack(ids_all), torch.stack(strong_all), w)
     for k, ((s, e), be) in enumerate(zip(plan, backends)):
-        fin = be.finalize(torch.from_numpy(merged[k]).to(labels.device))
-        final[s:e].copy_(fin)
+        final[s:e].copy_(be.finalize(merged[k]))
     return final
 
 
@@ -158,21 +186,37 @@ def canny_bands_local(frame_u8, nbands: int, weights, low: float, high: float):
         be.classify_trace(frame_u8[lo:hi].contiguous(), s, h, weights, low, high)
         ids, strong = be.edges()
         backends.append(be)
-        ids_all.append(globalize_ids(ids.cpu().numpy(), k))
-        strong_all.append(strong.cpu().numpy())
-    merged = merge_edges(np.stack(ids_all), np.stack(strong_all), w)
+        ids_all.append(ids)
+        strong_all.append(strong)
+    merged = merge_edges_device(torch.stack(ids_all), torch.stack(strong_all), w)
     for k, ((s, e), be) in enumerate(zip(plan, backends)):
-        final[s:e].copy_(be.finalize(torch.from_numpy(merged[k]).to(frame_u8.device)))
+        final[s:e].copy_(be.finalize(merged[k]))
         labels[s:e].copy_(be.labels)
     return labels, final
 
 
+def band_buffer(rows: int, width: int, row0: int, full_height: int, radius: int, device=None):
+    """A band's HBM buffer with room for its halo rows: returns (buf, band),
+    band = buf[ht:ht+rows], the view the caller fills with its own rows once.
+    Passing buf as `staged` to distributed_band_canny then receives the halos
+    in place (no per-step copy of the band)."""
+    import torch
+
+    halo = halo_rows(radius)
+    ht, hb = min(halo, row0), min(halo, full_height - row0 - rows)
+    buf = torch.empty((ht + rows + hb, width), dtype=torch.uint8, device=device)
+    return buf, buf[ht:ht + rows]
+
+
 def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: float, high: float,
-                           backend=None, group=None):
+                           backend=None, group=None, staged=None):
     """One rank's share of a row-band-partitioned frame.
 
     band_u8: this rank's rows [row0, row0+rows) as a (rows, W) u8 tensor on the
     rank's device (CUDA under NCCL, CPU under gloo with a test backend).
+    staged: optional buffer from band_buffer() whose middle rows are band_u8;
+    the halos are received into it in place (otherwise the band is copied
+    into a fresh haloed buffer every call).
     Returns (labels, final) for those rows, equal to the rows of the
     whole-frame result."""
     import torch
@@ -182,14 +226,28 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     rows, w = band_u8.shape
     r = (len(weights) - 1) // 2
     halo = halo_rows(r)
-    # neighbour row counts are needed to know how many halo rows they can give
-    counts = [torch.zeros(2, dtype=torch.int64, device=band_u8.device) for _ in range(world)]
-    dist.all_gather(counts, torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), group=group)
-    meta = [(int(c[0]), int(c[1])) for c in counts]
+    be = backend if backend is not None else CudaBandBackend(rows, w)
+    # every rank's (row0, rows): how many halo rows each neighbour can give.
+    # Exchanged once per backend (a reused backend keeps it: no collective and
+    # no host sync per step)
+    key = (row0, rows, full_height, world)
+    cached = getattr(be, "band_meta", None)
+    if cached is not None and cached[0] == key:
+        meta = cached[1]
+    else:
+        counts = [torch.zeros(2, dtype=torch.int64, device=band_u8.device) for _ in range(world)]
+        dist.all_gather(counts, torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), group=group)
+        meta = [(int(c[0]), int(c[1])) for c in counts]
+        be.band_meta = (key, meta)
     ht = min(halo, row0)
     hb = min(halo, full_height - row0 - rows)
-    buf = torch.empty((ht + rows + hb, w), dtype=torch.uint8, device=band_u8.device)
-    buf[ht:ht + rows].copy_(band_u8)
+    if staged is not None:
+        if staged.shape != (ht + rows + hb, w) or staged[ht:ht + rows].data_ptr() != band_u8.data_ptr():
+            raise ValueError("staged must be band_buffer()'s buffer holding band_u8 as its middle rows")
+        buf = staged
+    else:
+        buf = torch.empty((ht + rows + hb, w), dtype=torch.uint8, device=band_u8.device)
+        buf[ht:ht + rows].copy_(band_u8)
     # halo exchange (a halo may span several thin neighbour bands)
     ops = []
     for peer in range(world):
@@ -206,14 +264,20 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
         if g0 < g1 and not (row0 <= g0 and g1 <= row0 + rows):
             dst = buf[g0 - (row0 - ht):g1 - (row0 - ht)]
             ops.append(dist.P2POp(dist.irecv, dst, peer, group))
-    recvd = []
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    del recvd
-    be = backend if backend is not None else CudaBandBackend(rows, w)
     be.classify_trace(buf, row0, full_height, weights, low, high)
     ids, strong = be.edges()
+    if hasattr(be, "merge"):
+        # device path: gather the edge rows device to device, merge on the device
+        ids_l = [torch.empty_like(ids) for _ in range(world)]
+        st_l = [torch.empty_like(strong) for _ in range(world)]
+        dist.all_gather(ids_l, ids, group=group)
+        dist.all_gather(st_l, strong, group=group)
+        merged = be.merge(torch.stack(ids_l), torch.stack(st_l))
+        return be.labels, be.finalize(merged[rank])
+    # host path (backends without a device merge): globalised ids, host union-find
     gids = torch.from_numpy(globalize_ids(ids.cpu().numpy(), rank)).to(band_u8.device)
     ids_l = [torch.empty_like(gids) for _ in range(world)]
     st_l = [torch.empty_like(strong) for _ in range(world)]

@@ -834,6 +834,22 @@ int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows,
     return EF_OK;
 }
 
+size_t ef_band_merge_scratch_bytes(int32_t nbands, int32_t width) {
+    if (nbands < 1 || width < 1 || (long long)nbands * 2 * width > (1ll << 30)) return 0;
+    return band_merge_scratch_bytes(nbands, width);
+}
+
+int ef_band_merge_device(int32_t nbands, int32_t width, const int64_t* d_ids, const uint8_t* d_strong,
+                         uint8_t* d_strong_out, void* d_scratch, size_t scratch_bytes, void* stream) {
+    const size_t need = ef_band_merge_scratch_bytes(nbands, width);
+    if (!need) return fail(EF_EINVAL, "bad band merge dimensions");
+    if (!d_ids || !d_strong || !d_strong_out || !d_scratch) return fail(EF_EINVAL, "NULL buffer");
+    if (scratch_bytes < need) return fail(EF_EINVAL, "band merge scratch too small");
+    EF_CHECK(launch_band_merge(nbands, width, d_ids, d_strong, d_strong_out, d_scratch, (cudaStream_t)stream),
+             "band merge");
+    return EF_OK;
+}
+
 int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width, const uint8_t* d_labels,
                      uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream) {
     int rc;

@@ -246,7 +246,11 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
         const float d = c - sqrt_apx(nmax);
         const bool amb = fabsf(uu) <= P.e_sec || fabsf(vv) <= P.e_sec;
         // threshold class: 2 / 1 / 0, or -1 inside a certification band
-        const int cls = c > P.hi_hi ? 2 : (c >= P.hi_lo ? -1 : (c > P.lo_hi ? 1 : (c >= P.lo_lo ? -1 : 0)));
+        // (as c > hi_hi ? 2 : c >= hi_lo ? -1 : c > lo_hi ? 1 : c >= lo_lo ? -1 : 0,
+        // with lo_lo <= lo_hi and hi_lo <= hi_hi; written as two selects over
+        // four compares so no lane branches on its pixel's class)
+        const int lo_cls = c >= P.lo_lo ? (c > P.lo_hi ? 1 : -1) : 0;
+        const int cls = c >= P.hi_lo ? (c > P.hi_hi ? 2 : -1) : lo_cls;
         const bool need_nms = cls >= 0 && (uint32_t)cls != cls0;
         const bool flag = cls < 0 || (need_nms && (amb || fabsf(d) <= P.e_nms));
         const uint32_t lab = flag ? (uint32_t)kFlag : ((need_nms && d > P.e_nms) ? (uint32_t)cls : cls0);

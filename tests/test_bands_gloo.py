@@ -58,6 +58,19 @@ class OracleBandBackend:
         return torch.from_numpy(merged[self.comp])
 
 
+class OracleBandBackendWithMerge(OracleBandBackend):
+    """Takes distributed_band_canny's device-path branch (gather band-local
+    edge rows, backend.merge) with the host union-find standing in for
+    ef_band_merge_device."""
+
+    def merge(self, ids_all, strong_all):
+        from paper_1710_07745_b200 import bands
+
+        nb = ids_all.shape[0]
+        gids = np.stack([bands.globalize_ids(ids_all[k].numpy(), k) for k in range(nb)])
+        return torch.from_numpy(bands.merge_edges(gids, strong_all.numpy(), self.width))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -66,7 +79,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, frame, weights, low, high, out):
+def _worker(rank, world, port, frame, weights, low, high, out, with_merge=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -75,9 +88,15 @@ def _worker(rank, world, port, frame, weights, low, high, out):
 
         plan = bands.band_plan(frame.shape[0], world)
         s, e = plan[rank]
-        band = torch.from_numpy(np.ascontiguousarray(frame[s:e]))
-        lab, fin = bands.distributed_band_canny(band, s, frame.shape[0], weights, low, high,
-                                                backend=OracleBandBackend(e - s, frame.shape[1]))
+        staged = None
+        if with_merge:  # the in-place halo buffer (bench.py's layout)
+            staged, band = bands.band_buffer(e - s, frame.shape[1], s, frame.shape[0], (len(weights) - 1) // 2)
+            band.copy_(torch.from_numpy(np.ascontiguousarray(frame[s:e])))
+        else:
+            band = torch.from_numpy(np.ascontiguousarray(frame[s:e]))
+        lab, fin = bands.distributed_band_canny(band, s, frame.shape[0], weights, low, high, staged=staged,
+                                                backend=(OracleBandBackendWithMerge if with_merge else
+                                                         OracleBandBackend)(e - s, frame.shape[1]))
         out[rank] = (s, e, lab.numpy().copy(), fin.numpy().astype(np.uint8).copy())
     finally:
         dist.destroy_process_group()
@@ -93,8 +112,8 @@ def _snake_frame(h, w):
     return img
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_band_canny_gloo(world):
+@pytest.mark.parametrize("world,with_merge", [(2, False), (3, False), (3, True)])
+def test_distributed_band_canny_gloo(world, with_merge):
     from paper_1710_07745_b200 import synth
 
     frames = [synth.config4(256, tile=64), _snake_frame(97, 80)]
@@ -103,7 +122,7 @@ def test_distributed_band_canny_gloo(world):
         manager = mp.Manager()
         out = manager.dict()
         port = _free_port()
-        mp.spawn(_worker, args=(world, port, frame, weights, 20.0, 50.0, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, frame, weights, 20.0, 50.0, out, with_merge), nprocs=world, join=True)
         el, ef_ = O.canny(frame, weights, 20.0, 50.0)
         lab = np.zeros_like(el)
         fin = np.zeros_like(el)

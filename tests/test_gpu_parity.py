@@ -297,6 +297,39 @@ def test_band_paths_match_whole_frame(canny):
         assert np.array_equal(_np(got).astype(bool), ref), plan
 
 
+def test_device_band_merge_matches_host_merge(canny):
+    """ef_band_merge_device (band-local ids, union-find on the GPU) against the
+    host ef_band_merge on globalised ids: random edge rows with heavy id reuse
+    (components spanning many columns), empty bands, one band, width 1, and a
+    chain crossing every seam."""
+    from paper_1710_07745_b200 import bands
+
+    rng = np.random.default_rng(11)
+    cases = []
+    for nb, w, nid, p_bg in [(2, 64, 5, 0.3), (8, 1000, 40, 0.5), (5, 1, 2, 0.2), (1, 77, 9, 0.1),
+                             (16, 4096, 3000, 0.6), (3, 50, 50, 1.0), (8, 16384, 200, 0.9)]:
+        ids = rng.integers(0, nid, size=(nb, 2 * w)).astype(np.int64) * 7 + 3  # sparse, large local ids
+        ids[rng.random((nb, 2 * w)) < p_bg] = -1
+        strong = (rng.random((nb, 2 * w)) < 0.05).astype(np.uint8)
+        strong[ids < 0] = 0
+        cases.append((ids, strong))
+    # one component snaking through every seam, strong only in the last band
+    nb, w = 6, 32
+    ids = np.full((nb, 2 * w), -1, np.int64)
+    strong = np.zeros((nb, 2 * w), np.uint8)
+    for k in range(nb):
+        ids[k, 5] = ids[k, w + 6] = 100 + k  # top x=5 and bottom x=6 are one band-local component
+    strong[nb - 1, 5] = 1
+    cases.append((ids, strong))
+    for ids, strong in cases:
+        nb, w = ids.shape[0], ids.shape[1] // 2
+        gids = np.stack([bands.globalize_ids(ids[k], k) for k in range(nb)])
+        want = bands.merge_edges(gids, strong, w)
+        got = _np(bands.merge_edges_device(_dev(ids), _dev(strong), w))
+        assert np.array_equal(got, want), (nb, w)
+    assert want[0, 5] == 1  # the snake's strong pixel reached the first band
+
+
 def test_host_buffer_entry_matches_device(canny):
     frames = synth.config3(3, 256)
     w = O.gaussian_weights(1.4, radius=2)
