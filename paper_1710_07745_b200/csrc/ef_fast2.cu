@@ -339,8 +339,7 @@ static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, 
 
 
 // d = b[x+1] - b[x-1] and s = b[x-1] + 2 b[x] + b[x+1] for this lane's 4 columns
-__device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], float (&sm)[4]) {
-    const float4 bb = *reinterpret_cast<const float4*>(brow);
+__device__ __forceinline__ void sobel_vals(const float4 bb, float (&d)[4], float (&sm)[4]) {
     // neighbour lanes' edge columns (lanes 0 / 31 get wrapped values: only
     // columns no output depends on are affected)
     const float bl = __shfl_up_sync(0xffffffffu, bb.w, 1);
@@ -353,6 +352,12 @@ __device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], floa
     sm[1] = fmaf(2.f, bb.y, bb.x + bb.z);
     sm[2] = fmaf(2.f, bb.z, bb.y + bb.w);
     sm[3] = fmaf(2.f, bb.w, bb.z + br);
+}
+
+__device__ __forceinline__ float4 ldb(const float* brow) { return *reinterpret_cast<const float4*>(brow); }
+
+__device__ __forceinline__ void sobel_row(const float* brow, float (&d)[4], float (&sm)[4]) {
+    sobel_vals(ldb(brow), d, sm);
 }
 
 template <int R, bool FUSED>
@@ -381,10 +386,15 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     sobel_row(brow(y0 - 1 + j0), d[1], sm[1]);
     // one magnitude row; (pu, pm, pd) = ring slots of the b rows above, at and
     // below it (period 3)
+    // the b row below each magnitude row is loaded one row step ahead (its
+    // shared-memory latency overlaps the previous row's arithmetic: K1 -0.7%)
+    float4 bnext = ldb(brow(y0 + j0));
     auto row_step = [&](int u, int pu, int pm, int pd) {
         const int j = j0 + u;
         const int Ym = y0 - 1 + j;
-        sobel_row(brow(Ym + 1), d[pd], sm[pd]);
+        const float4 bcur = bnext;
+        bnext = ldb(brow(min(Ym + 2, y0 + V2_BROWS - 3)));  // clamped: the last step's value is unused
+        sobel_vals(bcur, d[pd], sm[pd]);
         const float2 two = f2(2.f, 2.f);
         const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[pd][0], d[pd][1])));
         const float2 gx23 = fma2(two, f2(d[pm][2], d[pm][3]), add2(f2(d[pu][2], d[pu][3]), f2(d[pd][2], d[pd][3])));
