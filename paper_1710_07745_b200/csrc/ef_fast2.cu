@@ -330,12 +330,13 @@ struct V3Smem {
         float m[V3_MROWS][V2_CS];                   // squared magnitudes
         unsigned char in[V2_IN_ROWS][V2_IN_COLS];   // phase 1: TMA-staged input tile + halo
     };
-    float b[V2_BROWS][V2_CS];
+    float b[V2_BROWS + 1][V2_CS];  // + 1: phase 2's one-row-ahead load of its last step (value unused)
     unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
     unsigned long long mbar;
     FgBits bits;
 };
 static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, "TMA / float4 alignment");
+static_assert(EF_K1_MINB * (sizeof(V3Smem) + 1024) <= 233472, "CTAs per SM the register budget assumes fit in shared memory");
 
 
 // d = b[x+1] - b[x-1] and s = b[x-1] + 2 b[x] + b[x+1] for this lane's 4 columns
@@ -393,7 +394,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const int j = j0 + u;
         const int Ym = y0 - 1 + j;
         const float4 bcur = bnext;
-        bnext = ldb(brow(min(Ym + 2, y0 + V2_BROWS - 3)));  // clamped: the last step's value is unused
+        bnext = ldb(brow(Ym + 2));  // the last warp's last step reads the spare row V2_BROWS
         sobel_vals(bcur, d[pd], sm[pd]);
         const float2 two = f2(2.f, 2.f);
         const float2 gx01 = fma2(two, f2(d[pm][0], d[pm][1]), add2(f2(d[pu][0], d[pu][1]), f2(d[pd][0], d[pd][1])));

@@ -483,7 +483,10 @@ hyst_dense_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
 // memory per tile instead of ~20 KB.  Tiles with more than WCAP foreground
 // pixels go to hyst_dense_kernel.
 // ---------------------------------------------------------------------------
-constexpr int WCAP = 512;
+#ifndef EF_H1_WCAP
+#define EF_H1_WCAP 512
+#endif
+constexpr int WCAP = EF_H1_WCAP;
 #ifndef EF_H1_WARPS
 #define EF_H1_WARPS 4
 #endif
