@@ -406,7 +406,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 10 * args.steps,  # ws_begin, K1, 2 fix-up, 2 H1, merge, resolve, 2 finalize
+            "gpu_launches": 8 * args.steps,  # ws_begin, K1, fix-up, H1, dense H1, merge, resolve, finalize
             "stats": {k: int(v) for k, v in stats.items()},
         }
         print(json.dumps(line), flush=True)

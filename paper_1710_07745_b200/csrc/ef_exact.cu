@@ -229,57 +229,51 @@ __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, un
     if (lab == 2) atomicOr(&B.st[w], 1ull << (x & 63));
 }
 
+// Fix-ups: every flagged pixel recomputed exactly, one warp per pixel.  The
+// normal case walks K1's fix list; when the list overflowed, the same launch
+// scans every label byte for flags instead (one kernel either way: a separate
+// always-launched fallback kernel cost a ~3 us slot in the PDL chain).
 __global__ void __launch_bounds__(FX_WARPS * 32)
-fix_list_kernel(const uint8_t* __restrict__ src, FrameGeom g, ExactParams P, uint8_t* labels,
-                const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
+fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P, uint8_t* labels,
+           const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
     __shared__ double s_b[FX_WARPS][25];
     __shared__ double s_m[FX_WARPS][11];
     pdl_wait();
     pdl_trigger();
-    const int warp = threadIdx.x >> 5;
-    unsigned long long n = hdr->fix_count;
-    if (n > hdr->fix_cap) n = hdr->fix_cap;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * FX_WARPS + warp; e < n;
-         e += (unsigned long long)gridDim.x * FX_WARPS) {
-        unsigned long long idx = list[e], f;
-        int y, x;
-        out_coords(idx, g, f, y, x);
-        fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
-                       labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
-        fix_bits(B, g, f, y, x, labels[idx], labels + idx);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)&hdr->stats.fixups, hdr->fix_count);
-}
-
-// Overflow path: the fix list was too small; scan every label byte.
-__global__ void __launch_bounds__(FX_WARPS * 32)
-fix_scan_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P,
-                uint8_t* labels, WsHeader* hdr, FgBits B) {
-    __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
-    __shared__ double s_b[FX_WARPS][25];
-    __shared__ double s_m[FX_WARPS][11];
-    pdl_wait();
-    pdl_trigger();
-    if (!hdr->overflow) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned long long total = (unsigned long long)batch * g.rows * g.W;
-    for (unsigned long long base = ((unsigned long long)blockIdx.x * FX_WARPS + warp) * 32; base < total;
-         base += (unsigned long long)gridDim.x * FX_WARPS * 32) {
-        unsigned long long idx = base + lane;
-        bool flagged = idx < total && (labels[idx] & kFlag);
-        unsigned mask = __ballot_sync(0xffffffffu, flagged);
-        while (mask) {
-            int l = __ffs(mask) - 1;
-            mask &= mask - 1;
-            unsigned long long p = base + l, f;
+    if (!hdr->overflow) {
+        const unsigned long long n = hdr->fix_count;  // <= fix_cap without overflow
+        for (unsigned long long e = (unsigned long long)blockIdx.x * FX_WARPS + warp; e < n;
+             e += (unsigned long long)gridDim.x * FX_WARPS) {
+            unsigned long long idx = list[e], f;
             int y, x;
-            out_coords(p, g, f, y, x);
+            out_coords(idx, g, f, y, x);
             fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
-                           labels + p, (unsigned long long*)&hdr->stats.ambiguous);
-            fix_bits(B, g, f, y, x, labels[p], labels + p);
+                           labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
+            fix_bits(B, g, f, y, x, labels[idx], labels + idx);
+        }
+    } else {
+        // overflow: the list is incomplete; scan every label byte
+        const unsigned long long total = (unsigned long long)batch * g.rows * g.W;
+        for (unsigned long long base = ((unsigned long long)blockIdx.x * FX_WARPS + warp) * 32; base < total;
+             base += (unsigned long long)gridDim.x * FX_WARPS * 32) {
+            unsigned long long idx = base + lane;
+            bool flagged = idx < total && (labels[idx] & kFlag);
+            unsigned mask = __ballot_sync(0xffffffffu, flagged);
+            while (mask) {
+                int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                unsigned long long p = base + l, f;
+                int y, x;
+                out_coords(p, g, f, y, x);
+                fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
+                               labels + p, (unsigned long long*)&hdr->stats.ambiguous);
+                fix_bits(B, g, f, y, x, labels[p], labels + p);
+            }
         }
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)&hdr->stats.fixups, hdr->fix_count);
 }
 
 // ---------------------------------------------------------------------------
@@ -310,11 +304,8 @@ template cudaError_t launch_exact<double>(const double*, int64_t, int, int, cons
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
                        int sm_count, cudaStream_t st) {
-    cudaError_t e = launch_pdl(fix_list_kernel, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, g, P, labels,
-                               list, hdr, B);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(fix_scan_kernel, dim3(sm_count * 4), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, hdr,
-                      B);
+    return launch_pdl(fix_kernel, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, list,
+                      hdr, B);
 }
 
 }  // namespace ef

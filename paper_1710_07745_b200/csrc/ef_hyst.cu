@@ -956,36 +956,34 @@ __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr)
     }
 }
 
-// H4: pixels of undecided border components read their root's strong flag.
-__global__ void hyst_final_list_kernel(uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
-    pdl_wait();
-    pdl_trigger();
-    // on overflow the list is incomplete (chunks past the cap were dropped) and
-    // hyst_final_tile_kernel finalises every pending tile instead
-    if (hdr->plist_overflow) return;
-    // grid (x, PL_STRIPES): blockIdx.y is the stripe
-    const unsigned long long n = min(b.plist_count[blockIdx.y], b.plist_scap);
-    const unsigned long long base = (unsigned long long)blockIdx.y * b.plist_scap;
-    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (unsigned long long)gridDim.x * blockDim.x)
-        if (b.gstrong[gfind_ro(b.gpar, b.plist_node[base + k])]) final_out[b.plist_idx[base + k]] = 1;
-}
-
 struct TileCCL;
 __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
                                 uint8_t* __restrict__ final_out, const HystBufs& b, long long tile, TileCCL& s);
 
-// H4 fallback when the pending list overflowed: re-run the tile CCL for every
-// pending tile (same deterministic CCL, so the same nodes).
+// H4: pixels of undecided border components read their root's strong flag,
+// from the pending list.  When the list overflowed (chunks past the cap were
+// dropped) the same launch re-runs the tile CCL for every pending tile instead
+// (same deterministic CCL, so the same nodes): one kernel either way, no
+// always-launched fallback kernel in the PDL chain.
+// Grid (x, PL_STRIPES), H_THREADS threads: list mode reads stripe blockIdx.y;
+// overflow mode walks the tiles over the flattened grid.
 __global__ void __launch_bounds__(H_THREADS)
-hyst_final_tile_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, int frames,
-                       uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
+hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, int frames,
+                  uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
-    if (!hdr->plist_overflow) return;
+    if (!hdr->plist_overflow) {
+        const unsigned long long n = min(b.plist_count[blockIdx.y], b.plist_scap);
+        const unsigned long long base = (unsigned long long)blockIdx.y * b.plist_scap;
+        for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+             k += (unsigned long long)gridDim.x * blockDim.x)
+            if (b.gstrong[gfind_ro(b.gpar, b.plist_node[base + k])]) final_out[b.plist_idx[base + k]] = 1;
+        return;
+    }
     const long long ntiles = (long long)tiles_x * tiles_y * frames;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long nblocks = (long long)gridDim.x * gridDim.y;
+    for (long long tile = (long long)blockIdx.y * gridDim.x + blockIdx.x; tile < ntiles; tile += nblocks) {
         if (b.pending[tile]) hyst_final_tile(labels, H, W, tiles_x, tiles_y, final_out, b, tile, s);
     }
 }
@@ -1092,14 +1090,9 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
 
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
-    cudaError_t e = launch_pdl(hyst_final_list_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES),
-                               dim3(256), 0, st, final_out, b, hdr);
-    if (e != cudaSuccess) return e;
     HystLayout L = hyst_layout(batch, H, W);
-    e = launch_pdl(hyst_final_tile_kernel, dim3(sm_count * 2), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x,
-                   L.tiles_y, (int)batch, final_out, b, hdr);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    return launch_pdl(hyst_final_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), dim3(H_THREADS), 0,
+                      st, labels, H, W, L.tiles_x, L.tiles_y, (int)batch, final_out, b, hdr);
 }
 
 cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
