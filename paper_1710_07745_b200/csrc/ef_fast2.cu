@@ -284,25 +284,28 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // TMA: the u8 tile + halo (144 columns x TH+4+2R rows of frame z) lands in
-// shared memory in one bulk tensor copy; completion on an mbarrier.
+// shared memory in one bulk tensor copy; completion on an mbarrier.  Thread 0
+// issues it first thing (tma_issue), so the CTA's prologue runs while the
+// tile is in flight; everyone waits in tma_wait.
 template <int R, class Smem>
-__device__ __forceinline__ void tma_stage(Smem& S, const CUtensorMap& tmap, int xv0, int y0, const FrameGeom& g) {
+__device__ __forceinline__ void tma_issue(Smem& S, const CUtensorMap& tmap, int xv0, int y0, const FrameGeom& g) {
     constexpr int rows = V2_BROWS + 2 * R;
     const uint32_t bar = smem_u32(&S.mbar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // init visible to the TMA unit
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * V2_IN_COLS)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-                "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
-                "r"(bar)
-            : "memory");
-    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // init visible to the TMA unit
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * V2_IN_COLS)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
+            "r"(bar)
+        : "memory");
+}
+
+template <class Smem>
+__device__ __forceinline__ void tma_wait(Smem& S) {
+    __syncthreads();  // the mbarrier's initialisation is visible to every thread
+    const uint32_t bar = smem_u32(&S.mbar);
     uint32_t done = 0;
     while (!done) {
         asm volatile(
@@ -519,10 +522,11 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     V3Smem& S = *reinterpret_cast<V3Smem*>(smraw);
     pdl_wait();  // workspace counters and bit planes are reset by the previous kernel
     pdl_trigger();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x0 = blockIdx.x * V2Cfg<R>::OW;
     const int xv0 = x0 - V2Cfg<R>::HXA;
     const int y0 = g.out0 + blockIdx.y * V2_TH;
+    if (use_tma && threadIdx.x == 0) tma_issue<R>(S, tmap, xv0, y0, g);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
     const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
     if (threadIdx.x == 0) S.bits = B;
@@ -538,7 +542,7 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         const int xa = xv0 & ~15, yin = y0 - 2 - R;
         const int ylo = max(0, g.g0), yhi = min(FH, g.g0 + g.H) - 1;  // frame rows present in the buffer
         if (use_tma) {
-            tma_stage<R>(S, tmap, xv0, y0, g);
+            tma_wait(S);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
                 replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
