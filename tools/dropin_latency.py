@@ -21,8 +21,8 @@ for radius in (None, 2):
 
 # breakdown
 from paper_1710_07745_b200 import canny
-import oracle.oracle as O
-w = O.gaussian_weights(1.4)
+from paper_1710_07745_b200.filtering import build_gaussian_kernel
+w = build_gaussian_kernel(1.4).weights
 t0 = time.perf_counter()
 for _ in range(20):
     u8 = img.as_u8()

@@ -3,11 +3,11 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1710_07745_b200 import canny, synth
-import oracle.oracle as O
+from paper_1710_07745_b200.filtering import build_gaussian_kernel
 
 frames = synth.make_config(1)
 b, h, wd = frames.shape
-w = O.gaussian_weights(1.4, radius=2)
+w = build_gaussian_kernel(1.4, radius=2).weights
 hsrc = torch.from_numpy(frames).pin_memory()
 hlab = torch.empty_like(hsrc).pin_memory(); hfin = torch.empty_like(hsrc).pin_memory()
 plab = np.empty(frames.shape, np.uint8); pfin = np.empty(frames.shape, np.uint8)

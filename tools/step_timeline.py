@@ -5,11 +5,11 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1710_07745_b200 import canny, synth, _lib
-import oracle.oracle as O
+from paper_1710_07745_b200.filtering import build_gaussian_kernel
 
 frames = torch.from_numpy(synth.make_config(1)).cuda()
 b, h, w = frames.shape
-wt = O.gaussian_weights(1.4, radius=2)
+wt = build_gaussian_kernel(1.4, radius=2).weights
 lab = torch.empty_like(frames); fin = torch.empty_like(frames)
 ws = canny.new_workspace(b, h, w, device=frames.device)
 lib = _lib.load(); _, wp, r = canny.host_weights(wt)
