@@ -59,6 +59,13 @@ typedef struct ef_stats {
     int64_t pending_tiles;    /* tiles finalised after the global merge         */
 } ef_stats;
 
+/* Which capacity fallbacks the last call on this workspace took (synchronises
+ * `stream`): h_out[0] fix list overflowed (FX scanned every label), [1] a
+ * pending-list stripe overflowed (H4 re-ran the pending tiles), [2] tiles H1's
+ * warp kernel handed to the block kernel, [3] a node-list stripe overflowed (H3
+ * scanned every perimeter slot).  For tests and diagnostics. */
+int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream, uint32_t* h_out);
+
 /* Bytes of device workspace needed by ef_canny_u8 / ef_canny_f64 /
  * ef_trace_edges for `batch` frames of height x width. */
 size_t ef_workspace_bytes(int64_t batch, int32_t height, int32_t width);

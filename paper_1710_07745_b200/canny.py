@@ -270,6 +270,14 @@ def read_stats(ws, stream=None) -> dict:
     return st.as_dict()
 
 
+def read_paths(ws, stream=None) -> dict:
+    """Capacity fallbacks the last call on `ws` took (ef_read_paths)."""
+    out = (ctypes.c_uint32 * 4)()
+    _lib.check(_lib.load().ef_read_paths(_ptr(ws), ws.numel(), _stream_ptr(stream), out), "ef_read_paths")
+    return {"fix_overflow": bool(out[0]), "pending_overflow": bool(out[1]), "dense_tiles": int(out[2]),
+            "node_overflow": bool(out[3])}
+
+
 def reset_stats(ws, stream=None) -> None:
     rc = _lib.load().ef_reset_stats(_ptr(ws), ws.numel(), _stream_ptr(stream))
     _lib.check(rc, "ef_reset_stats")

@@ -357,6 +357,18 @@ int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream,
     return EF_OK;
 }
 
+int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream, uint32_t* h_out) {
+    if (!d_workspace || workspace_bytes < sizeof(WsHeader) || !h_out) return fail(EF_EINVAL, "bad arguments");
+    EF_CHECK(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+    WsHeader h;
+    EF_CHECK(cudaMemcpy(&h, d_workspace, sizeof h, cudaMemcpyDeviceToHost), "header copy");
+    h_out[0] = h.overflow;
+    h_out[1] = h.plist_overflow;
+    h_out[2] = h.dense_count;
+    h_out[3] = h.node_overflow;
+    return EF_OK;
+}
+
 int ef_classify_u8(const uint8_t* d_src, int64_t batch, int32_t height, int32_t width,
                    const double* h_weights, int32_t radius, double low, double high, uint8_t* d_labels,
                    void* d_workspace, size_t workspace_bytes, void* stream) {

@@ -163,7 +163,12 @@ def test_dense_noise_overflow_paths(canny, low, high):
     frames = rng.integers(0, 256, size=(1, 2048, 2048), dtype=np.uint8)
     w = O.gaussian_weights(0.6, radius=1)
     el, ef_ = O.canny(frames, w, low, high)
-    lab, fin = canny.canny_u8(_dev(frames), w, low, high)
+    ws = canny.new_workspace(*frames.shape)
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high, ws=ws)
+    paths = canny.read_paths(ws)
+    # the fallbacks this test is for ran: block-kernel tiles always, the
+    # pending-list overflow at the lower threshold
+    assert paths["dense_tiles"] > 0 and paths["pending_overflow"] == (low < 5.0), paths
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
     lab2 = canny.classify_u8(_dev(frames), w, low, high)
@@ -181,7 +186,9 @@ def test_fix_list_overflow_on_threshold_ties(canny, low, high):
     frames = np.kron(blk, np.ones((4, 4), np.uint8))[None]
     w = np.array([0.25, 0.5, 0.25])
     el, ef_ = O.canny(frames, w, low, high)
-    lab, fin = canny.canny_u8(_dev(frames), w, low, high)
+    ws = canny.new_workspace(*frames.shape)
+    lab, fin = canny.canny_u8(_dev(frames), w, low, high, ws=ws)
+    assert canny.read_paths(ws)["fix_overflow"]  # the full-scan fix-up ran
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
 
@@ -193,7 +200,9 @@ def test_node_list_overflow_large_noise(canny):
     frames = rng.integers(0, 256, size=(1, 8192, 8192), dtype=np.uint8)
     w = O.gaussian_weights(0.6, radius=1)
     el, ef_ = O.canny(frames, w, 5.0, 60.0)
-    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0)
+    ws = canny.new_workspace(*frames.shape)
+    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)
+    assert canny.read_paths(ws)["node_overflow"]  # H3's perimeter-scan fallback ran
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
 
