@@ -59,6 +59,12 @@ typedef struct ef_stats {
     int64_t pending_tiles;    /* tiles finalised after the global merge         */
 } ef_stats;
 
+/* Hysteresis tuning (process-wide): launches with at most tiles_per_sm 64x64
+ * tiles per SM run the tile pass with one 128-thread block per tile instead of
+ * one warp per tile (few, large tiles: C0, C2).  Default 32; 0 = always one
+ * warp per tile.  The result is identical either way. */
+int ef_set_block_tile_threshold(int32_t tiles_per_sm);
+
 /* Which capacity fallbacks the last call on this workspace took (synchronises
  * `stream`): h_out[0] fix list overflowed (FX scanned every label), [1] a
  * pending-list stripe overflowed (H4 re-ran the pending tiles), [2] tiles H1's

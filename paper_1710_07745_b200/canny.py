@@ -270,6 +270,11 @@ def read_stats(ws, stream=None) -> dict:
     return st.as_dict()
 
 
+def set_block_tile_threshold(tiles_per_sm: int) -> None:
+    """Hysteresis tuning: block-per-tile at or below this many tiles per SM (0: never)."""
+    _lib.check(_lib.load().ef_set_block_tile_threshold(int(tiles_per_sm)), "ef_set_block_tile_threshold")
+
+
 def read_paths(ws, stream=None) -> dict:
     """Capacity fallbacks the last call on `ws` took (ef_read_paths)."""
     out = (ctypes.c_uint32 * 4)()

@@ -357,6 +357,12 @@ int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream,
     return EF_OK;
 }
 
+int ef_set_block_tile_threshold(int32_t tiles_per_sm) {
+    if (tiles_per_sm < 0) return fail(EF_EINVAL, "tiles_per_sm must be >= 0");
+    set_block_tile_threshold(tiles_per_sm);
+    return EF_OK;
+}
+
 int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream, uint32_t* h_out) {
     if (!d_workspace || workspace_bytes < sizeof(WsHeader) || !h_out) return fail(EF_EINVAL, "bad arguments");
     EF_CHECK(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");

@@ -1055,6 +1055,26 @@ HystLayout hyst_layout(int64_t batch, int H, int W) {
     return L;
 }
 
+// H1 for every tile with one 128-thread block per tile (label input): for
+// launches with few tiles, where one warp per tile leaves the SMs idle while
+// each warp walks a large tile's union-find alone.
+__global__ void __launch_bounds__(H_THREADS)
+hyst_all_block_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, long long ntiles,
+                      uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
+    __shared__ TileCCL s;
+    pdl_wait();
+    pdl_trigger();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        hyst_block_tile(labels, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+}
+
+// tiles per SM at or below which H1 runs one block per tile (ef_set_block_tile_threshold)
+// (initial value: EF_H1_BLOCK_TILES_PER_SM for measurement runs, else 32)
+static std::atomic<int> g_block_tiles_per_sm{getenv("EF_H1_BLOCK_TILES_PER_SM") ? atoi(getenv("EF_H1_BLOCK_TILES_PER_SM"))
+                                                                               : 32};
+
+void set_block_tile_threshold(int tiles_per_sm) { g_block_tiles_per_sm.store(tiles_per_sm); }
+
 cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
                               cudaStream_t st) {
@@ -1067,11 +1087,19 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
         if (r == cudaSuccess)
             r = cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(hyst_all_block_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
         return r;
     });
     if (e != cudaSuccess) return e;
+    const bool allblock = L.tiles <= (int64_t)g_block_tiles_per_sm.load() * sm_count;
     const dim3 wgrid((unsigned)((L.tiles_x * L.tiles_y + WT_WARPS - 1) / WT_WARPS), (unsigned)batch);
-    if (bits)
+    if (allblock) {
+        // few tiles: a block per tile (the dense-tile list stays empty)
+        e = launch_pdl(hyst_all_block_kernel, dim3((unsigned)std::min<int64_t>(L.tiles, 16ll * sm_count)),
+                           dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x, L.tiles_y, (long long)L.tiles, final_out,
+                           b, hdr);
+    } else if (bits)
         e = launch_pdl(hyst_local_warp_kernel<true>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
                        L.tiles_y, final_out, b, hdr, *bits);
     else

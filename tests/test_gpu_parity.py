@@ -23,6 +23,16 @@ def canny():
     return c
 
 
+@pytest.fixture(params=[0, 32], ids=["warp-per-tile", "block-per-tile-when-few"])
+def h1_path(request, canny):
+    """Both hysteresis tile passes: 0 = always one warp per tile (with the dense
+    tile hand-over), 32 = the default (one block per tile for launches with at
+    most 32 tiles per SM)."""
+    canny.set_block_tile_threshold(request.param)
+    yield request.param
+    canny.set_block_tile_threshold(32)
+
+
 def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
@@ -34,7 +44,7 @@ def _np(t):
 # ---------------------------------------------------------------- golden ----
 @pytest.mark.parametrize("cfg", range(5))
 @pytest.mark.parametrize("r", [2, 5])
-def test_configs_match_reference_golden(canny, cfg, r):
+def test_configs_match_reference_golden(canny, cfg, r, h1_path):
     g = load("configs.npz")
     frames = synth.make_config(cfg, reduced=True)
     assert synth.sha256_u8(frames) == str(g[f"c{cfg}/sha256"])
@@ -92,7 +102,7 @@ def _random_image(rng, h, w, kind):
 
 
 @pytest.mark.parametrize("r", [0, 1, 2, 3, 4, 5, 6, 7, 8, 15])
-def test_fast_path_random_vs_oracle(canny, r):
+def test_fast_path_random_vs_oracle(canny, r, h1_path):
     rng = np.random.default_rng(100 + r)
     sigma = max(0.3, r / 3.0)
     w = O.gaussian_weights(sigma, radius=r)
@@ -155,7 +165,7 @@ def test_workspace_reuse_across_inputs_and_shapes(canny):
 
 
 @pytest.mark.parametrize("low,high", [(5.0, 100.0), (2.0, 400.0)])
-def test_dense_noise_overflow_paths(canny, low, high):
+def test_dense_noise_overflow_paths(canny, low, high, h1_path):
     """Dense noise with low thresholds: tiles beyond the warp kernel's capacity
     (block-kernel path), node and pending-list stripes that overflow (perimeter
     scan / tile re-run fallbacks) -- all must still equal the oracle."""
@@ -166,9 +176,10 @@ def test_dense_noise_overflow_paths(canny, low, high):
     ws = canny.new_workspace(*frames.shape)
     lab, fin = canny.canny_u8(_dev(frames), w, low, high, ws=ws)
     paths = canny.read_paths(ws)
-    # the fallbacks this test is for ran: block-kernel tiles always, the
-    # pending-list overflow at the lower threshold
-    assert paths["dense_tiles"] > 0 and paths["pending_overflow"] == (low < 5.0), paths
+    # the fallbacks this test is for ran: the pending-list overflow at the lower
+    # threshold, and (one warp per tile) the hand-over of dense tiles to the block kernel
+    assert paths["pending_overflow"] == (low < 5.0), paths
+    assert (paths["dense_tiles"] > 0) == (h1_path == 0), paths
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
     lab2 = canny.classify_u8(_dev(frames), w, low, high)
@@ -276,7 +287,7 @@ def _spiral_labels(n):
     return lab
 
 
-def test_hysteresis_vs_oracle(canny):
+def test_hysteresis_vs_oracle(canny, h1_path):
     rng = np.random.default_rng(3)
     cases = [_snake(300, 257), _spiral_labels(333), _snake(64, 64), _snake(65, 129)]
     for p in ([0.55, 0.35, 0.10], [0.3, 0.65, 0.05], [0.9, 0.09, 0.01]):
