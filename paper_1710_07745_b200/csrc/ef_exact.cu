@@ -143,18 +143,41 @@ ex_tile_kernel(const In* __restrict__ src, int H, int W, ExactParams P, uint8_t*
 // ---------------------------------------------------------------------------
 constexpr int FX_WARPS = 4;
 
+constexpr int FX_WIN = 2 * kMaxR + 5;  // input window side: rows / columns a fix-up reads
+
 __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom& g, int y, int x,
-                               const ExactParams& P, double* s_h, double* s_b, double* s_m, uint8_t* out,
-                               unsigned long long* ambiguous) {
+                               const ExactParams& P, uint8_t* s_in, double* s_h, double* s_b, double* s_m,
+                               uint8_t* out, unsigned long long* ambiguous) {
     const int lane = threadIdx.x & 31;
     const int r = P.r, H = g.full_H, W = g.W;
     const int hy0 = clampi(y - 2 - r, 0, H - 1), hy1 = clampi(y + 2 + r, 0, H - 1);
     const int nhr = hy1 - hy0 + 1;
+    // the input window, staged with every load of a batch issued before any is
+    // stored (one L2 round trip per 8 bytes a lane needs, instead of one per
+    // tap of a dependent multiply-add chain): rows [hy0, hy1], columns [c0, c1]
+    // = every column clamp(clamp(x - 2 + i) - r + j) can name
+    const int c0 = max(0, clampi(x - 2, 0, W - 1) - r), c1 = min(W - 1, clampi(x + 2, 0, W - 1) + r);
+    const int ncols = c1 - c0 + 1, nwin = nhr * ncols;
+    for (int base = 0; base < nwin; base += 8 * 32) {
+        uint8_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = base + q * 32 + lane;
+            const int row = k / ncols;
+            v[q] = k < nwin ? img[(size_t)(hy0 + row - g.g0) * W + c0 + (k - row * ncols)] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = base + q * 32 + lane;
+            if (k < nwin) s_in[k] = v[q];
+        }
+    }
+    __syncwarp();
     // h(Y', clamp(x - 2 + i)) for Y' in [hy0, hy1], i in 0..4  (filtering.py:52-54)
     for (int k = lane; k < nhr * 5; k += 32) {
         int row = k / 5, i = k - row * 5;
-        int Y = hy0 + row, X = clampi(x - 2 + i, 0, W - 1);
-        const uint8_t* p = img + (size_t)(Y - g.g0) * W;
+        int X = clampi(x - 2 + i, 0, W - 1);
+        const uint8_t* p = s_in + row * ncols - c0;  // p[c] = input(hy0 + row, c) for c in [c0, c1]
         double acc = __dmul_rn(P.w[0], (double)p[clampi(X - r, 0, W - 1)]);
         for (int j = 1; j <= 2 * r; ++j)
             acc = __dadd_rn(acc, __dmul_rn(P.w[j], (double)p[clampi(X - r + j, 0, W - 1)]));
@@ -237,6 +260,7 @@ __global__ void __launch_bounds__(FX_WARPS * 32)
 fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P, uint8_t* labels,
            const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
     __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
+    __shared__ uint8_t s_in[FX_WARPS][FX_WIN * FX_WIN];
     __shared__ double s_b[FX_WARPS][25];
     __shared__ double s_m[FX_WARPS][11];
     pdl_wait();
@@ -249,7 +273,7 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
             unsigned long long idx = list[e], f;
             int y, x;
             out_coords(idx, g, f, y, x);
-            fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
+            fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
                            labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
             fix_bits(B, g, f, y, x, labels[idx], labels + idx);
         }
@@ -267,7 +291,7 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
                 unsigned long long p = base + l, f;
                 int y, x;
                 out_coords(p, g, f, y, x);
-                fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_h[warp], s_b[warp], s_m[warp],
+                fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
                                labels + p, (unsigned long long*)&hdr->stats.ambiguous);
                 fix_bits(B, g, f, y, x, labels[p], labels + p);
             }
