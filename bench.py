@@ -259,7 +259,7 @@ def run_bands(args):
     if rank == 0:
         line = {"metric": METRIC, "value": round(H * W / 1e6 / (ms / 1e3), 3), "unit": "MP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "fp32 certified + f64 fix-up (u8 in, u8 out)",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
                 "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
                 "config": {"workload": f"C4: one {H}x{W} frame, row bands over {world} GPU(s)",
                            "radius": args.radius, "thresholds": [low, high],
@@ -383,7 +383,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32 certified + f64 fix-up (u8 in, u8 out)",
+            "vs_baseline": None, "dtype": "f32", "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
             "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
             "config": {"workload": name, "frames_per_gpu": int(b), "height": int(h), "width": int(wd),
                        "radius": args.radius, "sigma": 1.4, "thresholds": [low, high],
