@@ -379,7 +379,8 @@ def run_ours(args):
     alg_bytes = 3 * px
     achieved = alg_bytes / (k1_ms / 1e3) / 1e9
     if rank == 0:
-        cpu = None if args.no_cpu else cpu_baseline(frames, w, low, high)
+        # the CPU baseline is timed on rank 0 at N=1 only (a reported baseline, not per-rank work)
+        cpu = None if (args.no_cpu or world > 1) else cpu_baseline(frames, w, low, high)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
