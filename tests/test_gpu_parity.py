@@ -256,6 +256,42 @@ def test_batch_of_frames_vs_oracle(canny):
         assert np.array_equal(_np(f1)[0], _np(fin)[i])
 
 
+def test_concurrent_calls_from_host_threads(canny):
+    """Distinct runs may run concurrently (one orchestrating thread per run):
+    four host threads, each with its own stream and workspace, issue fused calls
+    on different frame sizes at once; every result equals the oracle."""
+    import threading
+
+    w = O.gaussian_weights(1.4, radius=2)
+    shapes = [(2, 135, 241), (1, 300, 512), (3, 97, 160), (1, 512, 128)]
+    inputs = [synth.config1(*sh) for sh in shapes]
+    want = [O.canny(f, w, 20.0, 50.0, threads=4) for f in inputs]
+    got, errors = [None] * len(shapes), []
+
+    def run(k):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                x = _dev(inputs[k])
+                ws = canny.new_workspace(*inputs[k].shape)
+                for _ in range(5):  # overlap several calls per thread
+                    lab, fin = canny.canny_u8(x, w, 20.0, 50.0, ws=ws, stream=st)
+                st.synchronize()
+                got[k] = (_np(lab), _np(fin))
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(len(shapes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (lab, fin), (el, ef_) in zip(got, want):
+        assert np.array_equal(lab, el)
+        assert np.array_equal(fin.astype(bool), ef_)
+
+
 # ----------------------------------------------------------- hysteresis -----
 def _snake(h, w):
     lab = np.zeros((h, w), np.uint8)
