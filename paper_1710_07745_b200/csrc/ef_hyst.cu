@@ -52,22 +52,34 @@ struct TileCCL {
 __device__ __forceinline__ bool info_strong(unsigned v) { return !(v & 0x8000u); }
 __device__ __forceinline__ unsigned info_slot(unsigned v) { return v & NO_SLOT; }
 
+// info[] entries are 16-bit fields of 32-bit shared-memory words; the updates
+// go through shared-space atomics on the containing word (the word address is
+// formed as a shared-window address: an integer-cast generic pointer made the
+// compiler emit generic atomics, which are slower on shared memory)
+__device__ __forceinline__ uint32_t info_word(const unsigned short* p, int& sh) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    sh = (a & 2u) ? 16 : 0;
+    return a & ~3u;
+}
+
 __device__ __forceinline__ void info_set_strong(unsigned short* p) {
-    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
-    atomicAnd(w, ~(0x8000u << sh));
+    int sh;
+    const uint32_t w = info_word(p, sh);
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(w), "r"(~(0x8000u << sh)) : "memory");
 }
 
 // lower the slot field to v (CAS on the containing 32-bit word)
 __device__ __forceinline__ void info_min_slot(unsigned short* p, unsigned v) {
-    unsigned int* w = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-    const int sh = (reinterpret_cast<uintptr_t>(p) & 2) ? 16 : 0;
-    unsigned int old = *w;
+    int sh;
+    const uint32_t w = info_word(p, sh);
+    unsigned int old;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(old) : "r"(w) : "memory");
     while (true) {
         const unsigned cur = (old >> sh) & 0xffffu;
         if ((cur & NO_SLOT) <= v) return;
         const unsigned int nw = (old & ~(0xffffu << sh)) | (((cur & ~NO_SLOT) | v) << sh);
-        const unsigned int seen = atomicCAS(w, old, nw);
+        unsigned int seen;
+        asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(seen) : "r"(w), "r"(old), "r"(nw) : "memory");
         if (seen == old) return;
         old = seen;
     }
