@@ -105,19 +105,28 @@ class ClockSampler:
     def _poll(self):
         nv = self.nv
         masks = {k: getattr(nv, v, 0) for k, v in self.REASONS.items()}
+        i = 0
         while not self.stop_evt.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.reasons |= {k for k, m in masks.items() if m and (r & m)}
+                if i % 4 == 0:  # throttle reasons: every 4th poll (the slower query)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.reasons |= {k for k, m in masks.items() if m and (r & m)}
             except Exception:  # noqa: BLE001
                 break
-            time.sleep(0.002)
+            i += 1
+            time.sleep(0.0005)
 
     def __exit__(self, *exc):
         self.stop_evt.set()
         if self.nv is not None:
             self.t.join(timeout=1)
+            try:  # the region's last reasons, read once after it
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= {k for k, v in self.REASONS.items()
+                                 if getattr(self.nv, v, 0) and (r & getattr(self.nv, v, 0))}
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self):
         if not self.samples:
