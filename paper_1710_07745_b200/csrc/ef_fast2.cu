@@ -267,10 +267,10 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
             else O.hdr->overflow = 1u;
         }
     }
-    *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0) = packed;
+    st_global_u32(O.labels + rowbase + xv0 + cc0, packed);
     if (FUSED) {
         // final = strong (kFlag bytes give 0: the fix-up writes them)
-        *reinterpret_cast<uint32_t*>(O.labels + rowbase + xv0 + cc0 + bits.fin_off) = (packed >> 1) & 0x01010101u;
+        st_global_u32(O.labels + rowbase + xv0 + cc0 + bits.fin_off, (packed >> 1) & 0x01010101u);
         // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
         const uint32_t lo = packed & 0x03030303u;
         const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;

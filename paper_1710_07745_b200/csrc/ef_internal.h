@@ -62,8 +62,17 @@ struct FgBits {
 __device__ __forceinline__ void fg_bits_or(const FgBits& B, unsigned long long f, int yo, int x, uint32_t fgn,
                                            uint32_t stn) {
     const unsigned long long w = f * B.frame_words + (unsigned long long)yo * B.words + (unsigned)(x >> 6);
-    if (fgn) atomicOr(&B.fg[w], (unsigned long long)fgn << (x & 63));
-    if (stn) atomicOr(&B.st[w], (unsigned long long)stn << (x & 63));
+    // global-space reductions (no return value): callers reach here through
+    // pointers the compiler cannot prove global (the classifier is out of line)
+    if (fgn)
+        asm volatile("red.global.or.b64 [%0], %1;" ::"l"(B.fg + w), "l"((unsigned long long)fgn << (x & 63)) : "memory");
+    if (stn)
+        asm volatile("red.global.or.b64 [%0], %1;" ::"l"(B.st + w), "l"((unsigned long long)stn << (x & 63)) : "memory");
+}
+
+// 4-byte global store (explicit state space: see fg_bits_or)
+__device__ __forceinline__ void st_global_u32(void* p, uint32_t v) {
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 #endif
 
