@@ -259,12 +259,25 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
     }
     const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * P.W;
     if (any_flag) {
+        // one list append per group (global-space ops: see fg_bits_or)
+        unsigned fm = 0, cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (((packed >> (8 * k)) & 0xffu) == kFlag) fm |= 1u << k;
+        cnt = __popc(fm);
+        unsigned long long slot, cap;
+        asm volatile("atom.global.add.u64 %0, [%1], %2;" : "=l"(slot) : "l"(&O.hdr->fix_count), "l"((unsigned long long)cnt)
+                     : "memory");
+        asm volatile("ld.global.u64 %0, [%1];" : "=l"(cap) : "l"(&O.hdr->fix_cap) : "memory");
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (((packed >> (8 * k)) & 0xffu) != kFlag) continue;
-            const unsigned long long slot = atomicAdd(&O.hdr->fix_count, 1ull);
-            if (slot < O.hdr->fix_cap) O.fix_list[slot] = rowbase + (unsigned long long)(xv0 + cc0 + k);
-            else O.hdr->overflow = 1u;
+            if (!((fm >> k) & 1u)) continue;
+            if (slot < cap)
+                asm volatile("st.global.u64 [%0], %1;" ::"l"(O.fix_list + slot),
+                             "l"(rowbase + (unsigned long long)(xv0 + cc0 + k)) : "memory");
+            else
+                st_global_u32(&O.hdr->overflow, 1u);
+            ++slot;
         }
     }
     st_global_u32(O.labels + rowbase + xv0 + cc0, packed);
