@@ -190,7 +190,7 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
 }
 
 // ---------------------------------------------------------------- phase 2 --
-// The few scalars the out-of-line classifier needs (kept in registers).
+// The few scalars the classifier needs (kept in registers).
 struct V2Cls {
     float lo_lo, lo_hi, hi_lo, hi_hi, e_nms, e_sec;
     int cls0;
@@ -466,7 +466,7 @@ __device__ __forceinline__ int select32(unsigned w, int n) {
 // found by a binary search over the prefix counts and a bit select -- so every
 // round classifies 32 groups with no queue in shared memory.
 template <int R, bool FUSED>
-__device__ __noinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
+__device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
                                          const V2Out O) {
     constexpr int NW = (V2_TH + V2_WARPS - 1) / V2_WARPS;  // candidate words per warp
     static_assert(NW <= 32, "one word per lane");

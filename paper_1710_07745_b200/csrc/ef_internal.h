@@ -62,8 +62,9 @@ struct FgBits {
 __device__ __forceinline__ void fg_bits_or(const FgBits& B, unsigned long long f, int yo, int x, uint32_t fgn,
                                            uint32_t stn) {
     const unsigned long long w = f * B.frame_words + (unsigned long long)yo * B.words + (unsigned)(x >> 6);
-    // global-space reductions (no return value): callers reach here through
-    // pointers the compiler cannot prove global (the classifier is out of line)
+    // global-space reductions (no return value): stated explicitly -- through
+    // pointers the compiler could not prove global (an out-of-line classifier)
+    // these compiled to generic atomics with shared-space checks (K1 +3%)
     if (fgn)
         asm volatile("red.global.or.b64 [%0], %1;" ::"l"(B.fg + w), "l"((unsigned long long)fgn << (x & 63)) : "memory");
     if (stn)

@@ -3,8 +3,8 @@
     python tools/k1_phases.py gpurun_out/prof_v11.ncu-rep
 
 Segments are the SASS ranges between K1's block barriers (phase 1 ends at the
-barrier before phase 2, etc.); the out-of-line classifier (phase 3) follows
-the kernel's EXIT.  Uses `ncu -i ... --page source --print-source sass --csv`.
+barrier before phase 2, etc.; phase 3, the classifier, is the segment after
+the last barrier; code placed after the kernel's EXIT is reported separately).  Uses `ncu -i ... --page source --print-source sass --csv`.
 """
 import csv
 import io
@@ -28,7 +28,7 @@ def main(rep, kernel="k1v3"):
             segs.append((name, *cur))
             cur = [0, 0]
             nbar += op.startswith("BAR")
-            name = "after EXIT (classifier, out of line)" if op == "EXIT" else f"after barrier {nbar}"
+            name = "after EXIT (out-of-line code)" if op == "EXIT" else f"after barrier {nbar}"
         cur[0] += n
         cur[1] += sm
     segs.append((name, *cur))
