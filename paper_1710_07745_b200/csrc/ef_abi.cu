@@ -147,9 +147,13 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs 
                                 unsigned long long nwords) {
     pdl_wait();  // the previous call's kernels on this stream read the same workspace
     pdl_trigger();
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+    // 16-byte stores (the planes start 256-byte aligned), then the odd last word
+    const unsigned long long n16 = nwords / 2;
+    uint4* p16 = reinterpret_cast<uint4*>(planes);
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
          i += (unsigned long long)gridDim.x * blockDim.x)
-        planes[i] = 0ull;
+        p16[i] = make_uint4(0u, 0u, 0u, 0u);
+    if ((nwords & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) planes[nwords - 1] = 0ull;
     if (blockIdx.x != 0) return;
     if (threadIdx.x == 0) {
         hdr->fix_count = 0;
@@ -167,7 +171,7 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs 
 }
 
 cudaError_t launch_ws_begin(const Ws& ws, const WsLayout& L, unsigned long long nwords, int sms, cudaStream_t st) {
-    const unsigned long long want = (nwords + 255) / 256;
+    const unsigned long long want = (nwords / 2 + 255) / 256;
     const unsigned blocks = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, 4ull * sms));
     return launch_pdl(ws_begin_kernel, dim3(blocks), dim3(256), 0, st, ws.hdr, L.fix_cap, ws.hb, ws.fgbits, nwords);
 }
