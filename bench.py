@@ -44,6 +44,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--bands", action="store_true", help="config 4: row-band partition across ranks")
+    p.add_argument("--peer", action="store_true",
+                   help="with --bands: halo rows read in place from the neighbours' HBM (CUDA IPC / NVLink), "
+                        "no halo exchange step")
     return p.parse_args()
 
 
@@ -252,13 +255,15 @@ def run_bands(args):
     st = torch.cuda.current_stream()
     be = bands.CudaBandBackend(s1 - s0, W)  # workspace and band metadata reused across steps
     for _ in range(args.warmup):
-        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=staged)
+        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=None if args.peer else staged,
+                                     peer=args.peer)
     torch.cuda.synchronize()
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(st)
     for _ in range(args.steps):
-        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=staged)
+        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=None if args.peer else staged,
+                                     peer=args.peer)
     stop.record(st)
     torch.cuda.synchronize()
     dist.barrier()
@@ -272,7 +277,9 @@ def run_bands(args):
                 "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
                 "config": {"workload": f"C4: one {H}x{W} frame, row bands over {world} GPU(s)",
                            "radius": args.radius, "thresholds": [low, high],
-                           "parallelism": f"{world} row bands, NCCL P2P halo + all_gather of edge ids, device seam merge"},
+                           "parallelism": f"{world} row bands, " + ("halo rows read in place from peer HBM (CUDA IPC)"
+                                                                      if args.peer else "NCCL P2P halo exchange")
+                                          + ", all_gather of edge ids, device seam merge"},
                 "e2e": None, "gpu_launches": None}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

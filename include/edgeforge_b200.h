@@ -177,6 +177,26 @@ int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t f
                      double high, uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
                      size_t workspace_bytes, void* stream);
 
+/* The same with the halo rows read IN PLACE from the neighbour bands (no
+ * exchange step): d_band holds this band's `rows` rows only; d_top points at
+ * the top_rows = min(row0, radius+2) frame rows just above the band (the last
+ * rows of the band above -- on another GPU, a peer pointer from ef_ipc_open,
+ * read over NVLink), d_bot at the bot_rows = min(full_height-row0-rows,
+ * radius+2) rows just below.  Needs width % 4 == 0 and radius <= 6.  Results
+ * equal ef_band_canny_u8 on the contiguous haloed buffer. */
+int ef_band_canny_u8_peer(const uint8_t* d_band, const uint8_t* d_top, int32_t top_rows, const uint8_t* d_bot,
+                          int32_t bot_rows, int32_t row0, int32_t rows, int32_t full_height, int32_t width,
+                          const double* h_weights, int32_t radius, double low, double high, uint8_t* d_labels,
+                          uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* CUDA IPC for the peer halos: export a device pointer (any address inside an
+ * allocation) as a 64-byte handle + offset; another process opens it (peer
+ * access enabled lazily) and gets a device pointer to the same bytes;
+ * ef_ipc_close releases the mapping (pass the base from ef_ipc_open). */
+int ef_ipc_export(const void* d_ptr, void* h_handle64, uint64_t* h_offset);
+int ef_ipc_open(const void* h_handle64, uint64_t offset, void** d_ptr_out, void** d_base_out);
+int ef_ipc_close(void* d_base);
+
 /* Band-local hysteresis only, for labels already computed (the per-band
  * labelling of trace_edges_parallel, hysteresis.py:97-101). */
 int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,

@@ -54,6 +54,10 @@ _SIGNATURES = {
     "ef_band_halo_rows": ([I32], ctypes.c_int),
     "ef_band_canny_u8": ([P, I32, I32, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
     "ef_band_trace": ([P, I32, I32, P, P, SZ, P], ctypes.c_int),
+    "ef_band_canny_u8_peer": ([P, P, I32, P, I32, I32, I32, I32, I32, P, I32, D, D, P, P, P, SZ, P], ctypes.c_int),
+    "ef_ipc_export": ([P, P, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
+    "ef_ipc_open": ([P, ctypes.c_uint64, ctypes.POINTER(P), ctypes.POINTER(P)], ctypes.c_int),
+    "ef_ipc_close": ([P], ctypes.c_int),
     "ef_band_edges": ([P, SZ, I32, I32, P, P, P], ctypes.c_int),
     "ef_band_merge": ([I32, I32, P, P, P], ctypes.c_int),
     "ef_band_merge_scratch_bytes": ([I32, I32], SZ),

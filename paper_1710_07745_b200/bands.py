@@ -116,6 +116,26 @@ class CudaBandBackend:
                                           self.ws.data_ptr(), self.ws.numel(), self._stream())
         _lib.check(rc, "ef_band_canny_u8")
 
+    def classify_trace_peer(self, band, top_ptr: int, top_rows: int, bot_ptr: int, bot_rows: int, row0: int,
+                            full_height: int, weights, low: float, high: float):
+        """band: this rank's rows only; the halo rows are read in place through
+        top_ptr / bot_ptr (neighbour bands, e.g. IPC-mapped peer HBM)."""
+        t = self.torch
+        self.labels = t.empty((self.rows, self.width), dtype=t.uint8, device=band.device)
+        self.final = t.empty_like(self.labels)
+        _, wp, r = self.canny.host_weights(weights)
+        rc = _lib.load().ef_band_canny_u8_peer(band.data_ptr(), top_ptr or None, top_rows, bot_ptr or None, bot_rows,
+                                               row0, self.rows, full_height, self.width, wp, r, float(low),
+                                               float(high), self.labels.data_ptr(), self.final.data_ptr(),
+                                               self.ws.data_ptr(), self.ws.numel(), self._stream())
+        _lib.check(rc, "ef_band_canny_u8_peer")
+
+    def close_peers(self):
+        for base in getattr(self, "peer_bases", []):
+            _lib.check(_lib.load().ef_ipc_close(base), "ef_ipc_close")
+        self.peer_bases = []
+        self.peer_ptrs = None
+
     def trace(self, labels):
         t = self.torch
         self.labels = labels
@@ -208,8 +228,76 @@ def band_buffer(rows: int, width: int, row0: int, full_height: int, radius: int,
     return buf, buf[ht:ht + rows]
 
 
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    import ctypes
+
+    h = (ctypes.c_ubyte * 64)()
+    off = ctypes.c_uint64()
+    _lib.check(_lib.load().ef_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "ef_ipc_export")
+    return bytes(h), int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map another process's buffer: (device pointer, mapping base to close)."""
+    import ctypes
+
+    h = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+    ptr, base = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(_lib.load().ef_ipc_open(h, offset, ctypes.byref(ptr), ctypes.byref(base)), "ef_ipc_open")
+    return int(ptr.value), int(base.value)
+
+
+def _gather(tensor, world, group):
+    """all_gather that also works for CUDA tensors under gloo (host staging)."""
+    import torch
+    import torch.distributed as dist
+
+    host = tensor.is_cuda and dist.get_backend(group) == "gloo"
+    src = tensor.cpu() if host else tensor
+    out = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(out, src, group=group)
+    return [o.to(tensor.device) for o in out] if host else out
+
+
+def _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group):
+    """Device pointers to the halo rows inside the neighbour bands (opened once
+    per backend and band buffer over CUDA IPC: NVLink peer memory when the
+    neighbour is another GPU)."""
+    import torch.distributed as dist
+
+    w = band_u8.shape[1]
+    key = (band_u8.data_ptr(), row0, rows, full_height, world)
+    if getattr(be, "peer_ptrs", None) is not None and be.peer_ptrs[0] == key:
+        return be.peer_ptrs[1:]
+    if getattr(be, "peer_ptrs", None) is not None:
+        be.close_peers()
+    objs = [None] * world
+    dist.all_gather_object(objs, ipc_export(band_u8), group=group)
+    ht, hb = min(halo, row0), min(halo, full_height - row0 - rows)
+    top = bot = 0
+    be.peer_bases = []
+    for peer, (p0, pr) in enumerate(meta):
+        if peer == rank:
+            continue
+        if ht and p0 + pr == row0:  # the band just above: its last ht rows
+            if pr < ht:
+                raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
+            ptr, base = ipc_open(*objs[peer])
+            be.peer_bases.append(base)
+            top = ptr + (pr - ht) * w
+        if hb and p0 == row0 + rows:  # the band just below: its first hb rows
+            if pr < hb:
+                raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
+            ptr, base = ipc_open(*objs[peer])
+            be.peer_bases.append(base)
+            bot = ptr
+    be.peer_ptrs = (key, top, ht, bot, hb)
+    return be.peer_ptrs[1:]
+
+
 def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: float, high: float,
-                           backend=None, group=None, staged=None):
+                           backend=None, group=None, staged=None, peer: bool = False):
     """One rank's share of a row-band-partitioned frame.
 
     band_u8: this rank's rows [row0, row0+rows) as a (rows, W) u8 tensor on the
@@ -217,6 +305,11 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     staged: optional buffer from band_buffer() whose middle rows are band_u8;
     the halos are received into it in place (otherwise the band is copied
     into a fresh haloed buffer every call).
+    peer: no halo exchange -- the classifier reads the neighbours' halo rows in
+    place from their HBM (CUDA IPC mappings of their band buffers, opened once;
+    NVLink loads between GPUs).  Every rank's band must stay at the same address
+    across calls; each call synchronises its stream and the group before the
+    read, so every band's rows are written first.
     Returns (labels, final) for those rows, equal to the rows of the
     whole-frame result."""
     import torch
@@ -235,12 +328,17 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     if cached is not None and cached[0] == key:
         meta = cached[1]
     else:
-        counts = [torch.zeros(2, dtype=torch.int64, device=band_u8.device) for _ in range(world)]
-        dist.all_gather(counts, torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), group=group)
+        counts = _gather(torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), world, group)
         meta = [(int(c[0]), int(c[1])) for c in counts]
         be.band_meta = (key, meta)
     ht = min(halo, row0)
     hb = min(halo, full_height - row0 - rows)
+    if peer:
+        top, ht_, bot, hb_ = _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group)
+        torch.cuda.current_stream(band_u8.device).synchronize()
+        dist.barrier(group=group)  # every band's rows are in HBM before anyone reads its halo
+        be.classify_trace_peer(band_u8, top, ht_, bot, hb_, row0, full_height, weights, low, high)
+        return _merge_and_finalize(be, band_u8, rank, world, group)
     if staged is not None:
         if staged.shape != (ht + rows + hb, w) or staged[ht:ht + rows].data_ptr() != band_u8.data_ptr():
             raise ValueError("staged must be band_buffer()'s buffer holding band_u8 as its middle rows")
@@ -268,14 +366,18 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     be.classify_trace(buf, row0, full_height, weights, low, high)
+    return _merge_and_finalize(be, band_u8, rank, world, group)
+
+
+def _merge_and_finalize(be, band_u8, rank, world, group):
+    import torch
+    import torch.distributed as dist
+
+    w = band_u8.shape[1]
     ids, strong = be.edges()
     if hasattr(be, "merge"):
         # device path: gather the edge rows device to device, merge on the device
-        ids_l = [torch.empty_like(ids) for _ in range(world)]
-        st_l = [torch.empty_like(strong) for _ in range(world)]
-        dist.all_gather(ids_l, ids, group=group)
-        dist.all_gather(st_l, strong, group=group)
-        merged = be.merge(torch.stack(ids_l), torch.stack(st_l))
+        merged = be.merge(torch.stack(_gather(ids, world, group)), torch.stack(_gather(strong, world, group)))
         return be.labels, be.finalize(merged[rank])
     # host path (backends without a device merge): globalised ids, host union-find
     gids = torch.from_numpy(globalize_ids(ids.cpu().numpy(), rank)).to(band_u8.device)

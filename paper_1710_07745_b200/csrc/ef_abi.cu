@@ -4,6 +4,8 @@
 // semantics (ValueError -> EF_EINVAL), the certified fp32 error bounds for the
 // fast path, workspace layout, kernel sequencing, the host-buffer pipeline and
 // the cross-band union-find.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -831,6 +833,80 @@ int ef_band_canny_u8(const uint8_t* d_src, int32_t row0, int32_t rows, int32_t f
     if ((rc = run_classify_u8(d_src, 1, g, h_weights, radius, low, high, d_labels, ws, L, st, d_final, &bits)))
         return rc;
     return run_trace(d_labels, 1, rows, width, d_final, ws, L, st, false, false, &bits);
+}
+
+int ef_band_canny_u8_peer(const uint8_t* d_band, const uint8_t* d_top, int32_t top_rows, const uint8_t* d_bot,
+                          int32_t bot_rows, int32_t row0, int32_t rows, int32_t full_height, int32_t width,
+                          const double* h_weights, int32_t radius, double low, double high, uint8_t* d_labels,
+                          uint8_t* d_final, void* d_workspace, size_t workspace_bytes, void* stream) {
+    int rc;
+    if ((rc = check_dims(1, rows, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
+    if (row0 < 0 || row0 + rows > full_height) return fail(EF_EINVAL, "band outside the frame");
+    if (!d_band || !d_labels || !d_final) return fail(EF_EINVAL, "NULL buffer");
+    const int halo = radius + 2;
+    const int ht = std::min(row0, halo), hb = std::min(full_height - row0 - rows, halo);
+    if (top_rows != ht || bot_rows != hb || (ht > 0 && !d_top) || (hb > 0 && !d_bot))
+        return fail(EF_EINVAL, "peer halos must hold min(row0, radius+2) rows above and "
+                               "min(full_height-row0-rows, radius+2) rows below the band");
+    FastParams FP = make_fast(h_weights, radius, low, high);
+    if (has_negative(h_weights, radius)) return fail(EF_EINVAL, "signed kernel on a band");
+    FrameGeom g{ht + rows + hb, width, row0 - ht, full_height, row0, rows};
+    g.top = ht > 0 ? d_top : nullptr;
+    g.bot = hb > 0 ? d_bot : nullptr;
+    // the halo rows are read in place by the classifier kernel (needs W % 4 == 0
+    // and radius <= 6 -- the production kernel; without peers the buffer is contiguous)
+    if ((g.top || g.bot) && !k1v2_supported(FP, g))
+        return fail(EF_EINVAL, "peer halos need width % 4 == 0 and radius <= 6");
+    WsLayout L = ws_layout(1, rows, width);
+    if ((rc = check_ws(d_workspace, workspace_bytes, L))) return rc;
+    Ws ws = ws_bind(d_workspace, L);
+    cudaStream_t st = (cudaStream_t)stream;
+    FgBits bits;
+    if ((rc = run_classify_u8(d_band, 1, g, h_weights, radius, low, high, d_labels, ws, L, st, d_final, &bits)))
+        return rc;
+    return run_trace(d_labels, 1, rows, width, d_final, ws, L, st, false, false, &bits);
+}
+
+// CUDA IPC of a device buffer (any pointer inside an allocation): the handle of
+// its allocation plus the offset, so another process can read it in place.
+int ef_ipc_export(const void* d_ptr, void* h_handle64, uint64_t* h_offset) {
+    if (!d_ptr || !h_handle64 || !h_offset) return fail(EF_EINVAL, "bad arguments");
+    static const auto range_fn = []() -> CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(p);
+        return nullptr;
+    }();
+    if (!range_fn) return fail(EF_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+        return fail(EF_EINVAL, "pointer is not inside a device allocation");
+    cudaIpcMemHandle_t h;
+    EF_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(h_handle64, &h, sizeof h);
+    *h_offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return EF_OK;
+}
+
+int ef_ipc_open(const void* h_handle64, uint64_t offset, void** d_ptr_out, void** d_base_out) {
+    if (!h_handle64 || !d_ptr_out || !d_base_out) return fail(EF_EINVAL, "bad arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, h_handle64, sizeof h);
+    void* base = nullptr;
+    EF_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    *d_base_out = base;
+    *d_ptr_out = static_cast<char*>(base) + offset;
+    return EF_OK;
+}
+
+int ef_ipc_close(void* d_base) {
+    if (!d_base) return fail(EF_EINVAL, "bad arguments");
+    EF_CHECK(cudaIpcCloseMemHandle(d_base), "cudaIpcCloseMemHandle");
+    return EF_OK;
 }
 
 int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,

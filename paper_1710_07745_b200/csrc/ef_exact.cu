@@ -164,7 +164,7 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
         for (int q = 0; q < 8; ++q) {
             const int k = base + q * 32 + lane;
             const int row = k / ncols;
-            v[q] = k < nwin ? img[(size_t)(hy0 + row - g.g0) * W + c0 + (k - row * ncols)] : 0;
+            v[q] = k < nwin ? frame_row(img, g, hy0 + row)[c0 + (k - row * ncols)] : 0;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {

@@ -310,7 +310,7 @@ __device__ __forceinline__ void tma_issue(Smem& S, const CUtensorMap& tmap, int 
                  : "memory");
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-            "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - g.g0), "r"((int)blockIdx.z),
+            "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - src_row0(g)), "r"((int)blockIdx.z),
             "r"(bar)
         : "memory");
 }
@@ -538,7 +538,11 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     const int x0 = blockIdx.x * V2Cfg<R>::OW;
     const int xv0 = x0 - V2Cfg<R>::HXA;
     const int y0 = g.out0 + blockIdx.y * V2_TH;
-    if (use_tma && threadIdx.x == 0) tma_issue<R>(S, tmap, xv0, y0, g);
+    // a tile whose input box reaches a peer band's rows stages them by loads
+    // (the tensor map covers this band's own buffer only)
+    const bool tma_tile = use_tma && !(g.top && y0 - 2 - R < g.out0) &&
+                          !(g.bot && y0 + V2_TH + 2 + R > g.out0 + g.rows);
+    if (tma_tile && threadIdx.x == 0) tma_issue<R>(S, tmap, xv0, y0, g);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
     const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
@@ -554,7 +558,7 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         constexpr int NIN = V2_BROWS + 2 * R;
         const int xa = xv0 & ~15, yin = y0 - 2 - R;
         const int ylo = max(0, g.g0), yhi = min(FH, g.g0 + g.H) - 1;  // frame rows present in the buffer
-        if (use_tma) {
+        if (tma_tile) {
             tma_wait(S);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
@@ -565,10 +569,11 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
             // clamped bytes where a word crosses the frame edge
             constexpr int QW = V2_IN_COLS / 4;
-            const bool al4 = (reinterpret_cast<uintptr_t>(img) & 3) == 0;
+            const bool al4 = ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(g.top) |
+                               reinterpret_cast<uintptr_t>(g.bot)) & 3) == 0;
             for (int i = threadIdx.x; i < NIN * QW; i += V2_THREADS) {
                 const int r = i / QW, c = 4 * (i - r * QW);
-                const uint8_t* row = img + (size_t)(min(max(yin + r, ylo), yhi) - g.g0) * W;
+                const uint8_t* row = frame_row(img, g, min(max(yin + r, ylo), yhi));
                 const int X = xa + c;
                 uint32_t v;
                 if (al4 && X >= 0 && X + 3 < W) {
@@ -617,7 +622,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 static bool make_src_map(CUtensorMap& tm, const uint8_t* src, int64_t batch, const FrameGeom& g, int R) {
     auto enc = tensor_map_encoder();
     if (!enc || (g.W % 16) != 0 || (reinterpret_cast<uintptr_t>(src) & 15) != 0) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)batch};
+    cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)src_rows(g), (cuuint64_t)batch};
     cuuint64_t strides[2] = {(cuuint64_t)g.W, (cuuint64_t)g.W * g.H};
     cuuint32_t box[3] = {(cuuint32_t)V2_IN_COLS, (cuuint32_t)(V2_BROWS + 2 * R), 1};
     cuuint32_t estr[3] = {1, 1, 1};

@@ -18,7 +18,27 @@ struct FrameGeom {
     int full_H;  // rows of the whole frame (clamping is against [0, full_H))
     int out0;    // first global row to classify
     int rows;    // rows to classify; output row (Y - out0)
+    // Peer halos (multi-GPU row bands, ef_band_canny_u8_peer): when set, the
+    // source buffer holds only rows [out0, out0 + rows); rows above come from
+    // `top` (first row = global row g0) and rows below from `bot` (first row =
+    // global row out0 + rows) -- neighbour bands read in place, over NVLink
+    // for another GPU's HBM.  nullptr: the source holds rows [g0, g0 + H).
+    const uint8_t* top = nullptr;
+    const uint8_t* bot = nullptr;
 };
+
+#ifdef __CUDACC__
+// first global row held at the source pointer
+__host__ __device__ __forceinline__ int src_row0(const FrameGeom& g) { return (g.top || g.bot) ? g.out0 : g.g0; }
+// rows addressable from the source pointer (the tensor map's extent)
+__host__ __device__ __forceinline__ int src_rows(const FrameGeom& g) { return (g.top || g.bot) ? g.rows : g.H; }
+// global row y (inside [g0, g0 + H)) of frame `img` (= source + frame offset)
+__device__ __forceinline__ const uint8_t* frame_row(const uint8_t* img, const FrameGeom& g, int y) {
+    if (g.top && y < g.out0) return g.top + (size_t)(y - g.g0) * g.W;
+    if (g.bot && y >= g.out0 + g.rows) return g.bot + (size_t)(y - g.out0 - g.rows) * g.W;
+    return img + (size_t)(y - src_row0(g)) * g.W;
+}
+#endif
 
 struct HystLayout {
     int tiles_x, tiles_y;
