@@ -145,6 +145,7 @@ constexpr int FX_WARPS = 4;
 
 constexpr int FX_WIN = 2 * kMaxR + 5;  // input window side: rows / columns a fix-up reads
 
+template <bool PEER>
 __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom& g, int y, int x,
                                const ExactParams& P, uint8_t* s_in, double* s_h, double* s_b, double* s_m,
                                uint8_t* out, unsigned long long* ambiguous) {
@@ -164,7 +165,7 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
         for (int q = 0; q < 8; ++q) {
             const int k = base + q * 32 + lane;
             const int row = k / ncols;
-            v[q] = k < nwin ? frame_row(img, g, hy0 + row)[c0 + (k - row * ncols)] : 0;
+            v[q] = k < nwin ? frame_row<PEER>(img, g, hy0 + row)[c0 + (k - row * ncols)] : 0;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -256,6 +257,7 @@ __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, un
 // normal case walks K1's fix list; when the list overflowed, the same launch
 // scans every label byte for flags instead (one kernel either way: a separate
 // always-launched fallback kernel cost a ~3 us slot in the PDL chain).
+template <bool PEER>
 __global__ void __launch_bounds__(FX_WARPS * 32)
 fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P, uint8_t* labels,
            const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
@@ -273,7 +275,7 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
             unsigned long long idx = list[e], f;
             int y, x;
             out_coords(idx, g, f, y, x);
-            fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
+            fix_pixel_warp<PEER>(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
                            labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
             fix_bits(B, g, f, y, x, labels[idx], labels + idx);
         }
@@ -291,7 +293,7 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
                 unsigned long long p = base + l, f;
                 int y, x;
                 out_coords(p, g, f, y, x);
-                fix_pixel_warp(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
+                fix_pixel_warp<PEER>(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
                                labels + p, (unsigned long long*)&hdr->stats.ambiguous);
                 fix_bits(B, g, f, y, x, labels[p], labels + p);
             }
@@ -328,8 +330,8 @@ template cudaError_t launch_exact<double>(const double*, int64_t, int, int, cons
 cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, const ExactParams& P,
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
                        int sm_count, cudaStream_t st) {
-    return launch_pdl(fix_kernel, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, list,
-                      hdr, B);
+    auto kern = (g.top || g.bot) ? fix_kernel<true> : fix_kernel<false>;
+    return launch_pdl(kern, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, list, hdr, B);
 }
 
 }  // namespace ef

@@ -300,7 +300,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // shared memory in one bulk tensor copy; completion on an mbarrier.  Thread 0
 // issues it first thing (tma_issue), so the CTA's prologue runs while the
 // tile is in flight; everyone waits in tma_wait.
-template <int R, class Smem>
+template <int R, bool PEER, class Smem>
 __device__ __forceinline__ void tma_issue(Smem& S, const CUtensorMap& tmap, int xv0, int y0, const FrameGeom& g) {
     constexpr int rows = V2_BROWS + 2 * R;
     const uint32_t bar = smem_u32(&S.mbar);
@@ -310,7 +310,7 @@ __device__ __forceinline__ void tma_issue(Smem& S, const CUtensorMap& tmap, int 
                  : "memory");
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-            "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - src_row0(g)), "r"((int)blockIdx.z),
+            "r"(smem_u32(&S.in[0][0])), "l"(&tmap), "r"(xv0 & ~15), "r"(y0 - 2 - R - src_row0<PEER>(g)), "r"((int)blockIdx.z),
             "r"(bar)
         : "memory");
 }
@@ -526,7 +526,7 @@ __device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_
     }
 }
 
-template <int R, bool FUSED>
+template <int R, bool FUSED, bool PEER = false>
 __global__ void __launch_bounds__(V2_THREADS, EF_K1_MINB)
 k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t* __restrict__ labels,
             unsigned long long* __restrict__ fix_list, WsHeader* __restrict__ hdr,
@@ -540,9 +540,9 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     const int y0 = g.out0 + blockIdx.y * V2_TH;
     // a tile whose input box reaches a peer band's rows stages them by loads
     // (the tensor map covers this band's own buffer only)
-    const bool tma_tile = use_tma && !(g.top && y0 - 2 - R < g.out0) &&
-                          !(g.bot && y0 + V2_TH + 2 + R > g.out0 + g.rows);
-    if (tma_tile && threadIdx.x == 0) tma_issue<R>(S, tmap, xv0, y0, g);
+    const bool tma_tile = use_tma && !(PEER && g.top && y0 - 2 - R < g.out0) &&
+                          !(PEER && g.bot && y0 + V2_TH + 2 + R > g.out0 + g.rows);
+    if (tma_tile && threadIdx.x == 0) tma_issue<R, PEER>(S, tmap, xv0, y0, g);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
     const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
@@ -569,11 +569,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
             // clamped bytes where a word crosses the frame edge
             constexpr int QW = V2_IN_COLS / 4;
-            const bool al4 = ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(g.top) |
-                               reinterpret_cast<uintptr_t>(g.bot)) & 3) == 0;
+            const bool al4 = ((reinterpret_cast<uintptr_t>(img) |
+                               (PEER ? reinterpret_cast<uintptr_t>(g.top) | reinterpret_cast<uintptr_t>(g.bot) : 0)) &
+                              3) == 0;
             for (int i = threadIdx.x; i < NIN * QW; i += V2_THREADS) {
                 const int r = i / QW, c = 4 * (i - r * QW);
-                const uint8_t* row = frame_row(img, g, min(max(yin + r, ylo), yhi));
+                const uint8_t* row = frame_row<PEER>(img, g, min(max(yin + r, ylo), yhi));
                 const int X = xa + c;
                 uint32_t v;
                 if (al4 && X >= 0 && X + 3 < W) {
@@ -638,12 +639,15 @@ static cudaError_t launch_r(const uint8_t* src, int64_t batch, const FrameGeom& 
                             cudaStream_t st) {
     // FUSED (bit planes + final map) is a compile-time variant: the per-row
     // checks would otherwise sit in the hottest loop
-    auto kern = B.fg ? k1v3_kernel<R, true> : k1v3_kernel<R, false>;
+    const bool peer = g.top || g.bot;
+    auto kern = peer ? (B.fg ? k1v3_kernel<R, true, true> : k1v3_kernel<R, false, true>)
+                     : (B.fg ? k1v3_kernel<R, true> : k1v3_kernel<R, false>);
     const int smem = (int)sizeof(V3Smem);
     static std::atomic<uint64_t> configured{0};
     cudaError_t e = once_per_device(configured, [&] {
         cudaError_t r = cudaSuccess;
-        for (auto k : {k1v3_kernel<R, true>, k1v3_kernel<R, false>}) {
+        for (auto k : {k1v3_kernel<R, true>, k1v3_kernel<R, false>, k1v3_kernel<R, true, true>,
+                       k1v3_kernel<R, false, true>}) {
             if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             // occupancy is shared-memory bound: ask for the largest carveout
             if (r == cudaSuccess)

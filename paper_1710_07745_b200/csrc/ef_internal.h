@@ -28,15 +28,22 @@ struct FrameGeom {
 };
 
 #ifdef __CUDACC__
+// Kernels reading input rows are compiled twice: PEER = false (one contiguous
+// source buffer: no peer checks anywhere in the code) and PEER = true (band
+// calls with peer halos).
 // first global row held at the source pointer
-__host__ __device__ __forceinline__ int src_row0(const FrameGeom& g) { return (g.top || g.bot) ? g.out0 : g.g0; }
+template <bool PEER>
+__host__ __device__ __forceinline__ int src_row0(const FrameGeom& g) { return PEER ? g.out0 : g.g0; }
 // rows addressable from the source pointer (the tensor map's extent)
 __host__ __device__ __forceinline__ int src_rows(const FrameGeom& g) { return (g.top || g.bot) ? g.rows : g.H; }
 // global row y (inside [g0, g0 + H)) of frame `img` (= source + frame offset)
+template <bool PEER>
 __device__ __forceinline__ const uint8_t* frame_row(const uint8_t* img, const FrameGeom& g, int y) {
-    if (g.top && y < g.out0) return g.top + (size_t)(y - g.g0) * g.W;
-    if (g.bot && y >= g.out0 + g.rows) return g.bot + (size_t)(y - g.out0 - g.rows) * g.W;
-    return img + (size_t)(y - src_row0(g)) * g.W;
+    if (PEER) {
+        if (g.top && y < g.out0) return g.top + (size_t)(y - g.g0) * g.W;
+        if (g.bot && y >= g.out0 + g.rows) return g.bot + (size_t)(y - g.out0 - g.rows) * g.W;
+    }
+    return img + (size_t)(y - src_row0<PEER>(g)) * g.W;
 }
 #endif
 
