@@ -143,13 +143,14 @@ ex_tile_kernel(const In* __restrict__ src, int H, int W, ExactParams P, uint8_t*
 // ---------------------------------------------------------------------------
 constexpr int FX_WARPS = 4;
 
-constexpr int FX_WIN = 2 * kMaxR + 5;  // input window side: rows / columns a fix-up reads
 
-template <bool PEER>
-__device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom& g, int y, int x,
-                               const ExactParams& P, uint8_t* s_in, double* s_h, double* s_b, double* s_m,
-                               uint8_t* out, unsigned long long* ambiguous) {
-    const int lane = threadIdx.x & 31;
+// One fix-up by a group of G lanes (G = 16: two pixels per warp in flight);
+// gl = lane within the group, gm = the group's lane mask.
+template <bool PEER, int G>
+__device__ void fix_pixel_group(const uint8_t* __restrict__ img, const FrameGeom& g, int y, int x,
+                                const ExactParams& P, uint8_t* s_in, double* s_h, double* s_b, double* s_m,
+                                uint8_t* out, unsigned long long* ambiguous, int gl, unsigned gm) {
+    const int lane = gl;
     const int r = P.r, H = g.full_H, W = g.W;
     const int hy0 = clampi(y - 2 - r, 0, H - 1), hy1 = clampi(y + 2 + r, 0, H - 1);
     const int nhr = hy1 - hy0 + 1;
@@ -159,23 +160,23 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
     // = every column clamp(clamp(x - 2 + i) - r + j) can name
     const int c0 = max(0, clampi(x - 2, 0, W - 1) - r), c1 = min(W - 1, clampi(x + 2, 0, W - 1) + r);
     const int ncols = c1 - c0 + 1, nwin = nhr * ncols;
-    for (int base = 0; base < nwin; base += 8 * 32) {
+    for (int base = 0; base < nwin; base += 8 * G) {
         uint8_t v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int k = base + q * 32 + lane;
+            const int k = base + q * G + lane;
             const int row = k / ncols;
             v[q] = k < nwin ? frame_row<PEER>(img, g, hy0 + row)[c0 + (k - row * ncols)] : 0;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int k = base + q * 32 + lane;
+            const int k = base + q * G + lane;
             if (k < nwin) s_in[k] = v[q];
         }
     }
-    __syncwarp();
+    __syncwarp(gm);
     // h(Y', clamp(x - 2 + i)) for Y' in [hy0, hy1], i in 0..4  (filtering.py:52-54)
-    for (int k = lane; k < nhr * 5; k += 32) {
+    for (int k = lane; k < nhr * 5; k += G) {
         int row = k / 5, i = k - row * 5;
         int X = clampi(x - 2 + i, 0, W - 1);
         const uint8_t* p = s_in + row * ncols - c0;  // p[c] = input(hy0 + row, c) for c in [c0, c1]
@@ -184,10 +185,10 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
             acc = __dadd_rn(acc, __dmul_rn(P.w[j], (double)p[clampi(X - r + j, 0, W - 1)]));
         s_h[k] = acc;
     }
-    __syncwarp();
+    __syncwarp(gm);
     // b(y - 2 + j, x - 2 + i) for in-frame positions  (filtering.py:60-62)
-    if (lane < 25) {
-        int j = lane / 5, i = lane - j * 5;
+    for (int q = lane; q < 25; q += G) {
+        int j = q / 5, i = q - j * 5;
         int Y = y - 2 + j, X = x - 2 + i;
         if (Y >= 0 && Y < H && X >= 0 && X < W) {
             double acc = __dmul_rn(P.w[0], s_h[(clampi(Y - r, 0, H - 1) - hy0) * 5 + i]);
@@ -196,7 +197,7 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
             s_b[j * 5 + i] = acc;
         }
     }
-    __syncwarp();
+    __syncwarp(gm);
     auto Bv = [&](int Y, int X) {
         return s_b[(clampi(Y, 0, H - 1) - (y - 2)) * 5 + (clampi(X, 0, W - 1) - (x - 2))];
     };
@@ -218,7 +219,7 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
             s_m[10] = gy;
         }
     }
-    __syncwarp();
+    __syncwarp(gm);
     if (lane == 0) {
         const double c = s_m[4];
         const int s = exact_sector(s_m[9], s_m[10], ambiguous);
@@ -228,7 +229,7 @@ __device__ void fix_pixel_warp(const uint8_t* __restrict__ img, const FrameGeom&
         const double t = (c >= m1 && c >= m2) ? c : 0.0;
         *out = classify_exact(t, P.low, P.high);  // nms.py:51-52, hysteresis.py:57-59
     }
-    __syncwarp();
+    __syncwarp(gm);
 }
 
 // output index -> (frame, global row, column)
@@ -244,8 +245,8 @@ __device__ __forceinline__ void out_coords(unsigned long long idx, const FrameGe
 
 // the fused pipeline's foreground bit planes for a fixed pixel
 __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, unsigned long long f, int y, int x,
-                                         uint8_t lab, uint8_t* lab_ptr) {
-    if (!B.fg || (threadIdx.x & 31) != 0) return;
+                                         uint8_t lab, uint8_t* lab_ptr, int gl) {
+    if (!B.fg || gl != 0) return;
     lab_ptr[B.fin_off] = lab == 2 ? 1 : 0;  // final = strong (weak pixels are decided by the hysteresis)
     if (lab != 1 && lab != 2) return;
     const unsigned long long w = f * B.frame_words + (unsigned long long)(y - g.out0) * B.words + (unsigned)(x >> 6);
@@ -253,49 +254,67 @@ __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, un
     if (lab == 2) atomicOr(&B.st[w], 1ull << (x & 63));
 }
 
-// Fix-ups: every flagged pixel recomputed exactly, one warp per pixel.  The
+// Fix-ups: every flagged pixel recomputed exactly by a group of 16 lanes (two
+// pixels per warp in flight: the f64 chain per pixel is latency-bound).  The
 // normal case walks K1's fix list; when the list overflowed, the same launch
 // scans every label byte for flags instead (one kernel either way: a separate
 // always-launched fallback kernel cost a ~3 us slot in the PDL chain).
+// Dynamic shared memory: per group the input window, h, b and m, sized by r.
+constexpr int FX_G = 16;
+constexpr int FX_GROUPS = FX_WARPS * 32 / FX_G;
+
+__host__ __device__ inline int fx_group_bytes(int r) {
+    const int side = 2 * r + 5;
+    return 8 * (side * 5 + 25 + 11) + ((side * side + 7) & ~7);
+}
+
 template <bool PEER>
 __global__ void __launch_bounds__(FX_WARPS * 32)
 fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactParams P, uint8_t* labels,
            const unsigned long long* __restrict__ list, WsHeader* hdr, FgBits B) {
-    __shared__ double s_h[FX_WARPS][(2 * kMaxR + 5) * 5];
-    __shared__ uint8_t s_in[FX_WARPS][FX_WIN * FX_WIN];
-    __shared__ double s_b[FX_WARPS][25];
-    __shared__ double s_m[FX_WARPS][11];
+    extern __shared__ __align__(16) unsigned char fx_smem[];
     pdl_wait();
     pdl_trigger();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
+    const int grp = threadIdx.x / FX_G, gl = lane & (FX_G - 1);
+    const unsigned gm = (lane < FX_G) ? 0x0000ffffu : 0xffff0000u;
+    const int side = 2 * P.r + 5;
+    unsigned char* base = fx_smem + (size_t)grp * fx_group_bytes(P.r);
+    double* s_h = reinterpret_cast<double*>(base);
+    double* s_b = s_h + side * 5;
+    double* s_m = s_b + 25;
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_m + 11);
+    auto fix_one = [&](unsigned long long idx) {
+        unsigned long long f;
+        int y, x;
+        out_coords(idx, g, f, y, x);
+        fix_pixel_group<PEER, FX_G>(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in, s_h, s_b, s_m,
+                                    labels + idx, (unsigned long long*)&hdr->stats.ambiguous, gl, gm);
+        fix_bits(B, g, f, y, x, labels[idx], labels + idx, gl);
+    };
     if (!hdr->overflow) {
         const unsigned long long n = hdr->fix_count;  // <= fix_cap without overflow
-        for (unsigned long long e = (unsigned long long)blockIdx.x * FX_WARPS + warp; e < n;
-             e += (unsigned long long)gridDim.x * FX_WARPS) {
-            unsigned long long idx = list[e], f;
-            int y, x;
-            out_coords(idx, g, f, y, x);
-            fix_pixel_warp<PEER>(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
-                           labels + idx, (unsigned long long*)&hdr->stats.ambiguous);
-            fix_bits(B, g, f, y, x, labels[idx], labels + idx);
-        }
+        for (unsigned long long e = (unsigned long long)blockIdx.x * FX_GROUPS + grp; e < n;
+             e += (unsigned long long)gridDim.x * FX_GROUPS)
+            fix_one(list[e]);
     } else {
-        // overflow: the list is incomplete; scan every label byte
+        // overflow: the list is incomplete; scan every label byte (a warp
+        // ballots 32 bytes, its two groups take the flagged ones alternately)
+        const int warp = threadIdx.x >> 5, half = lane / FX_G;
         const unsigned long long total = (unsigned long long)batch * g.rows * g.W;
-        for (unsigned long long base = ((unsigned long long)blockIdx.x * FX_WARPS + warp) * 32; base < total;
-             base += (unsigned long long)gridDim.x * FX_WARPS * 32) {
-            unsigned long long idx = base + lane;
-            bool flagged = idx < total && (labels[idx] & kFlag);
+        for (unsigned long long b0 = ((unsigned long long)blockIdx.x * FX_WARPS + warp) * 32; b0 < total;
+             b0 += (unsigned long long)gridDim.x * FX_WARPS * 32) {
+            const unsigned long long idx = b0 + lane;
+            const bool flagged = idx < total && (labels[idx] & kFlag);
             unsigned mask = __ballot_sync(0xffffffffu, flagged);
-            while (mask) {
-                int l = __ffs(mask) - 1;
+            while (mask) {  // warp-uniform
+                const int l0 = __ffs(mask) - 1;
                 mask &= mask - 1;
-                unsigned long long p = base + l, f;
-                int y, x;
-                out_coords(p, g, f, y, x);
-                fix_pixel_warp<PEER>(src + f * (unsigned long long)g.H * g.W, g, y, x, P, s_in[warp], s_h[warp], s_b[warp], s_m[warp],
-                               labels + p, (unsigned long long*)&hdr->stats.ambiguous);
-                fix_bits(B, g, f, y, x, labels[p], labels + p);
+                const int l1 = mask ? __ffs(mask) - 1 : -1;
+                if (mask) mask &= mask - 1;
+                const int mine = half ? l1 : l0;
+                if (mine >= 0) fix_one(b0 + mine);
+                __syncwarp();
             }
         }
     }
@@ -331,7 +350,9 @@ cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, co
                        uint8_t* labels, const unsigned long long* list, WsHeader* hdr, const FgBits& B,
                        int sm_count, cudaStream_t st) {
     auto kern = (g.top || g.bot) ? fix_kernel<true> : fix_kernel<false>;
-    return launch_pdl(kern, dim3(sm_count * 16), dim3(FX_WARPS * 32), 0, st, src, batch, g, P, labels, list, hdr, B);
+    const size_t smem = (size_t)FX_GROUPS * fx_group_bytes(P.r);
+    return launch_pdl(kern, dim3(sm_count * 16), dim3(FX_WARPS * 32), smem, st, src, batch, g, P, labels, list, hdr,
+                      B);
 }
 
 }  // namespace ef
