@@ -209,12 +209,12 @@ __device__ void fix_pixel_group(const uint8_t* __restrict__ img, const FrameGeom
     };
     // lanes 0..8: gradient magnitude at the 3x3 positions around the pixel
     // (clamped), in parallel -- the NMS needs the centre and two of them
-    if (lane < 9) {
-        const int dy = lane / 3 - 1, dx = lane % 3 - 1;
+    for (int q = lane; q < 9; q += G) {
+        const int dy = q / 3 - 1, dx = q % 3 - 1;
         double gx, gy;
         grad(clampi(y + dy, 0, H - 1), clampi(x + dx, 0, W - 1), gx, gy);
-        s_m[lane] = exact_mag(gx, gy);
-        if (lane == 4) {
+        s_m[q] = exact_mag(gx, gy);
+        if (q == 4) {
             s_m[9] = gx;
             s_m[10] = gy;
         }
@@ -260,7 +260,10 @@ __device__ __forceinline__ void fix_bits(const FgBits& B, const FrameGeom& g, un
 // scans every label byte for flags instead (one kernel either way: a separate
 // always-launched fallback kernel cost a ~3 us slot in the PDL chain).
 // Dynamic shared memory: per group the input window, h, b and m, sized by r.
-constexpr int FX_G = 16;
+#ifndef EF_FX_G
+#define EF_FX_G 16
+#endif
+constexpr int FX_G = EF_FX_G;  // lanes per fix-up
 constexpr int FX_GROUPS = FX_WARPS * 32 / FX_G;
 
 __host__ __device__ inline int fx_group_bytes(int r) {
@@ -277,7 +280,7 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const int grp = threadIdx.x / FX_G, gl = lane & (FX_G - 1);
-    const unsigned gm = (lane < FX_G) ? 0x0000ffffu : 0xffff0000u;
+    const unsigned gm = (FX_G == 32 ? 0xffffffffu : ((1u << FX_G) - 1u)) << (lane & ~(FX_G - 1));
     const int side = 2 * P.r + 5;
     unsigned char* base = fx_smem + (size_t)grp * fx_group_bytes(P.r);
     double* s_h = reinterpret_cast<double*>(base);
@@ -299,20 +302,22 @@ fix_kernel(const uint8_t* __restrict__ src, int64_t batch, FrameGeom g, ExactPar
             fix_one(list[e]);
     } else {
         // overflow: the list is incomplete; scan every label byte (a warp
-        // ballots 32 bytes, its two groups take the flagged ones alternately)
-        const int warp = threadIdx.x >> 5, half = lane / FX_G;
+        // ballots 32 bytes, its groups take the flagged ones in turn)
+        const int warp = threadIdx.x >> 5, sub = lane / FX_G;
         const unsigned long long total = (unsigned long long)batch * g.rows * g.W;
         for (unsigned long long b0 = ((unsigned long long)blockIdx.x * FX_WARPS + warp) * 32; b0 < total;
              b0 += (unsigned long long)gridDim.x * FX_WARPS * 32) {
             const unsigned long long idx = b0 + lane;
             const bool flagged = idx < total && (labels[idx] & kFlag);
             unsigned mask = __ballot_sync(0xffffffffu, flagged);
-            while (mask) {  // warp-uniform
-                const int l0 = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int l1 = mask ? __ffs(mask) - 1 : -1;
-                if (mask) mask &= mask - 1;
-                const int mine = half ? l1 : l0;
+            while (mask) {  // warp-uniform: one flagged byte per group per round
+                int mine = -1;
+#pragma unroll
+                for (int k = 0; k < 32 / FX_G; ++k) {
+                    const int l = mask ? __ffs(mask) - 1 : -1;
+                    if (mask) mask &= mask - 1;
+                    if (k == sub) mine = l;
+                }
                 if (mine >= 0) fix_one(b0 + mine);
                 __syncwarp();
             }
