@@ -1,19 +1,24 @@
 """Benchmark: Canny megapixels/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--radius 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--radius 2]
     python bench.py --impl reference ...     # the reference path on the host CPU
 
-Workload (N=1): BASELINE.json configs[1] -- a batch of 64 seeded synthetic
-1920x1080 u8 frames, Gaussian sigma 1.4 "5x5" (radius 2), Sobel 3x3,
-thresholds 20/50.  A step is the whole Canny path over the batch: fused
-classify kernel (+ exact fix-ups) and hysteresis, labels and final edges
-written to HBM.  Under torchrun each rank processes its own 64-frame batch
-(weak scaling, no data-path collective: frames are independent units).
+Workload (headline): BASELINE.json configs[3] -- the largest single-GPU
+config: 1024 seeded synthetic 1024x1024 u8 images, Gaussian sigma 1.4 "5x5"
+(radius 2), Sobel 3x3, thresholds 20/50.  A step is the whole Canny path over
+the batch: fused classify kernel (+ exact fix-ups) and hysteresis, labels and
+final edges written to HBM.  With --gpus N the fixed 1024-image batch is
+sharded 1024/N images per rank (frames are independent units, no data-path
+collective; "scaling": "strong").  `--gpus N` without torchrun re-launches
+itself under torch.distributed.run with N ranks.
 
-value  device-timed (CUDA events, max over ranks), inputs resident in HBM,
-       rotating over 3 input batches (3 x 133 MB > 126 MB L2).
+value  device-timed (CUDA events, max over ranks), inputs resident in HBM
+       (the 1 GiB input batch is 8x the 126 MB L2; shards under 3x L2 rotate
+       over several resident copies).
 e2e    the same work through the host-buffer C-ABI entry (ef_canny_u8_host):
-       pinned host frames in, pinned host labels + final out, copies timed.
+       pinned host frames in, host labels + final out, copies timed.
+extra  C1 (64 x 1080p, sharded 64/N) device value, and C4 (one 16384^2 frame,
+       row bands over the N ranks: NCCL halo exchange + device seam merge).
 """
 
 from __future__ import annotations
@@ -21,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import sys
 import threading
@@ -30,44 +36,54 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Canny megapixels/sec (1/2/4/8 B200) and fused-kernel HBM GB/s as % of roofline"
+L2_BYTES = 126 * 2**20
+DEFAULT_FRAMES = {1: 64, 3: 1024}
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    p.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     p.add_argument("--radius", type=int, default=2, help="Gaussian radius (configs' 5x5 = 2; reference default 5)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--frames", type=int, default=None, help="override batch size (configs 1 and 3)")
+    p.add_argument("--frames", type=int, default=None, help="override the total batch (configs 1 and 3)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--bands", action="store_true", help="config 4: row-band partition across ranks")
+    p.add_argument("--no-extra", action="store_true", help="skip the C1 / C4 secondary measurements")
+    p.add_argument("--bands", action="store_true", help="config 4 only: row-band partition across ranks")
     p.add_argument("--peer", action="store_true",
                    help="with --bands: halo rows read in place from the neighbours' HBM (CUDA IPC / NVLink), "
                         "no halo exchange step")
     return p.parse_args()
 
 
-def workload(args):
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous near-equal shard [lo, hi) of n frames for `rank` (engine.plan_bands style)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def workload(cfg: int, frames: int | None, rank: int = 0, world: int = 1):
+    """This rank's frames of config `cfg` (batched configs are sharded by frame index;
+    each frame depends only on its own seed, so shards concatenate to the full batch)."""
     from paper_1710_07745_b200 import synth
 
-    cfg = args.config
-    if cfg == 1:
-        n = args.frames or 64
-        frames = synth.config1(n)
-        name = f"C1: {n} x 1920x1080 u8 frames (seeded ramp + 50 polygons + N(0,5^2))"
-    elif cfg == 3:
-        n = args.frames or 1024
-        frames = synth.config3(n)
-        name = f"C3: {n} x 1024x1024 u8 images (value noise + 30 shapes + N(0,8^2))"
-    else:
-        frames = synth.make_config(cfg)
-        name = {0: "C0: 512x512 u8 (rects + disks + N(0,8^2))", 2: "C2: 4096x4096 u8 rings + spiral",
-                4: "C4: 16384x16384 u8 tiled shapes + spirals"}[cfg]
     low, high = synth.CONFIG_THRESHOLDS[cfg]
-    return frames, name, low, high
+    if cfg in (1, 3):
+        n = frames or DEFAULT_FRAMES[cfg]
+        lo, hi = shard(n, rank, world)
+        if cfg == 1:
+            arr = synth.config_range(1, lo, hi)
+            name = f"C1: {n} x 1920x1080 u8 frames (seeded ramp + 50 polygons + N(0,5^2))"
+        else:
+            arr = synth.config_range(3, lo, hi)
+            name = f"C3: {n} x 1024x1024 u8 images (value noise + 30 shapes + N(0,8^2))"
+        return arr, name, low, high, n
+    arr = synth.make_config(cfg)
+    name = {0: "C0: 512x512 u8 (rects + disks + N(0,8^2))", 2: "C2: 4096x4096 u8 rings + spiral",
+            4: "C4: 16384x16384 u8 tiled shapes + spirals"}[cfg]
+    return arr, name, low, high, len(arr)
 
 
 def dist_env():
@@ -75,6 +91,21 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> None:
+    """`python bench.py --gpus N` (no WORLD_SIZE): become torchrun with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 class ClockSampler:
@@ -146,18 +177,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel_prefix="void k1v3_kernel"):
+TRAFFIC_CAPTURES = {
+    # (config, frames, radius) -> committed ncu capture of K1's dram bytes for that bench command
+    (3, 1024, 2): "profiles/r02_k1_dram_c3.csv",
+    (1, 64, 2): "profiles/r01_k1v3_dram_64frames.csv",
+}
+
+
+def ncu_traffic(cfg, frames, radius, kernel_prefix="void k1v3_kernel"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
     kernel, from the committed ncu capture of this bench command
-    (profiles/r01_k1v3_dram_64frames.csv: `ncu --metrics ...dram__bytes_*...
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu`)."""
+    (`ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:k1v3
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-extra`)."""
     import csv
 
-    path = os.path.join(ROOT, "profiles", "r01_k1v3_dram_64frames.csv")
+    rel = TRAFFIC_CAPTURES.get((cfg, frames, radius))
+    if rel is None:
+        return None, None
     try:
-        rows = list(csv.reader(open(path)))
+        rows = list(csv.reader(open(os.path.join(ROOT, rel))))
     except OSError:
-        return None
+        return None, rel
     hdr, by = None, {}
     for r in rows:
         if r and r[0] == "ID":
@@ -166,14 +206,16 @@ def ncu_traffic(kernel_prefix="void k1v3_kernel"):
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
             if d["Kernel Name"].startswith(kernel_prefix) and d["Metric Name"].startswith("dram__bytes_"):
+                unit = d.get("Metric Unit", "byte")
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
                 by.setdefault(d["ID"], 0.0)
-                by[d["ID"]] += float(d["Metric Value"].replace(",", ""))
-    return round(sum(by.values()) / len(by)) if by else None
+                by[d["ID"]] += float(d["Metric Value"].replace(",", "")) * scale
+    return (round(sum(by.values()) / len(by)) if by else None), rel
 
 
 def cpu_baseline(frames, weights, low, high):
     """Oracle port (oracle/ef_oracle.c: the reference's float64 algorithm in
-    C) on the host cores, bounded sample."""
+    C) on the host cores, bounded sample (~5 s)."""
     from oracle import oracle as O
 
     cores = len(os.sched_getaffinity(0))
@@ -197,123 +239,80 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import oracle as O
 
-    frames, name, low, high = workload(args)
+    # a bounded sample of the workload per step (the first frames of the batch)
+    cfg = args.config
+    if cfg in (1, 3):
+        n_total = args.frames or DEFAULT_FRAMES[cfg]
+        fpx = {1: 1920 * 1080, 3: 1024 * 1024}[cfg]
+        per = max(1, min(n_total, int(140e6 // fpx)))
+        frames, name, low, high, _ = workload(cfg, per, 0, 1)
+        name = name.replace(f"{per} x", f"{n_total} x")
+    else:
+        frames, name, low, high, _ = workload(cfg, None)
     w = O.gaussian_weights(1.4, radius=args.radius)
     cores = len(os.sched_getaffinity(0))
-    # bounded sample per step so the whole run stays within minutes
-    per_step = frames if frames.size <= 140e6 else frames[: max(1, int(140e6 // frames[0].size))]
     for _ in range(args.warmup):
-        O.canny(per_step[:1], w, low, high, threads=cores)
+        O.canny(frames[:1], w, low, high, threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.canny(per_step, w, low, high, threads=cores)
+        O.canny(frames, w, low, high, threads=cores)
         times.append(time.perf_counter() - t0)
     ms = statistics.median(times) * 1e3
-    value = per_step.size / 1e6 / (ms / 1e3)
+    value = frames.size / 1e6 / (ms / 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, see synth.py)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, see synth.py)",
         "config": {"workload": name, "radius": args.radius, "thresholds": [low, high],
-                   "sample_frames_per_step": int(len(per_step))},
+                   "sample_frames_per_step": int(len(frames))},
         "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(per_step)} frames per step, C float64 oracle port "
-                                   f"(reference is pure Python; no compiled reference exists)"},
+                         "sample": f"{len(frames)} frames ({frames.size / 1e6:.0f} MP) of the workload per step, "
+                                   f"C float64 oracle port on {cores} threads (the reference is pure Python; "
+                                   f"no compiled reference exists)"},
         "e2e": {"value": round(value, 3), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_bands(args):
-    """Config 4 across ranks: one 16384^2 frame, row bands (one per GPU), halo
-    rows and band-edge component ids exchanged over NCCL (bands.py).  Total
-    work is fixed as N grows: "scaling": "strong"."""
-    import numpy as np
+def _max_over_ranks(x: float, dev, world: int) -> float:
     import torch
-    import torch.distributed as dist
 
-    from paper_1710_07745_b200 import bands, synth
-    from paper_1710_07745_b200.filtering import build_gaussian_kernel
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev) if world > 1 else dist.init_process_group(
-        "nccl", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533", device_id=dev)
-    frame = synth.config4() if not args.frames else synth.config4(args.frames * 1024, tile=256)
-    H, W = frame.shape
-    low, high = synth.CONFIG_THRESHOLDS[4]
-    w = build_gaussian_kernel(1.4, radius=args.radius).weights
-    s0, s1 = bands.band_plan(H, world)[rank]
-    staged, band = bands.band_buffer(s1 - s0, W, s0, H, args.radius, device=dev)
-    band.copy_(torch.from_numpy(np.ascontiguousarray(frame[s0:s1])))  # halo rows arrive in place each step
-    st = torch.cuda.current_stream()
-    be = bands.CudaBandBackend(s1 - s0, W)  # workspace and band metadata reused across steps
-    for _ in range(args.warmup):
-        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=None if args.peer else staged,
-                                     peer=args.peer)
-    torch.cuda.synchronize()
-    dist.barrier()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(st)
-    for _ in range(args.steps):
-        bands.distributed_band_canny(band, s0, H, w, low, high, backend=be, staged=None if args.peer else staged,
-                                     peer=args.peer)
-    stop.record(st)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([start.elapsed_time(stop) / args.steps], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    if rank == 0:
-        line = {"metric": METRIC, "value": round(H * W / 1e6 / (ms / 1e3), 3), "unit": "MP/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
-                "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
-                "config": {"workload": f"C4: one {H}x{W} frame, row bands over {world} GPU(s)",
-                           "radius": args.radius, "thresholds": [low, high],
-                           "parallelism": f"{world} row bands, " + ("halo rows read in place from peer HBM (CUDA IPC)"
-                                                                      if args.peer else "NCCL P2P halo exchange")
-                                          + ", all_gather of edge ids, device seam merge"},
-                "e2e": None, "gpu_launches": None}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
 
 
-def run_ours(args):
+def _barrier(world: int):
+    if world > 1:
+        import torch
+
+        torch.distributed.barrier()
+
+
+def measure_batch(frames, weights, low, high, steps, warmup, dev, world, sample_clocks=True):
+    """Device-timed fused Canny over this rank's frames: one ef_canny_u8 call
+    per step.  Returns ms per step (max over ranks), K1 (+fix-up) ms, stats, clocks."""
     import numpy as np
     import torch
 
     from paper_1710_07745_b200 import _lib, canny
 
-    rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    frames, name, low, high = workload(args)
-    from paper_1710_07745_b200.filtering import build_gaussian_kernel
-
-    w = build_gaussian_kernel(1.4, radius=args.radius).weights
     b, h, wd = frames.shape
     px = frames.size
-    nbuf = 3
-    srcs = [torch.from_numpy(np.roll(frames, k, axis=0).copy()).to(dev) for k in range(nbuf)]
+    # inputs larger than L2 (or rotated copies whose sum is): no step reads a cached input
+    nbuf = 1 if px >= 3 * L2_BYTES else 3
+    srcs = [torch.from_numpy(np.roll(frames, k, axis=0).copy() if k else frames).to(dev) for k in range(nbuf)]
     labels = torch.empty_like(srcs[0])
     final = torch.empty_like(srcs[0])
     ws = canny.new_workspace(b, h, wd, device=dev)
     st = torch.cuda.current_stream()
     lib = _lib.load()
-    _, wp, r = canny.host_weights(w)
+    _, wp, r = canny.host_weights(weights)
     sptr = int(st.cuda_stream)
 
     def step(i, ev=None):
@@ -328,89 +327,253 @@ def run_ours(args):
         if ev is not None:
             _lib.check(lib.ef_set_classify_events(None, None), "events")
 
-    for i in range(args.warmup):
+    for i in range(warmup):
         step(i)
     canny.reset_stats(ws)
     # K1's own duration is sampled on every EV_EVERY-th timed step: an event
     # recorded between two kernels of the PDL chain stops the classifier from
-    # launching early, which cost 2.4% of the step when every step carried them
+    # launching early (2.4% of a C1 step when every step carried them)
     EV_EVERY = 5
-    sampled = [i for i in range(args.steps) if i % EV_EVERY == 0]
+    sampled = [i for i in range(steps) if i % EV_EVERY == 0]
     evs = {i: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for i in sampled}
     for a, c in evs.values():  # torch creates the CUDA event on first record
         a.record(st)
         c.record(st)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
+    _barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
-        start.record(st)
-        for i in range(args.steps):
-            step(i, evs.get(i))
-        stop.record(st)
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    total_ms = start.elapsed_time(stop)
+    clk = ClockSampler(dev.index) if sample_clocks else None
+    if clk:
+        clk.__enter__()
+    start.record(st)
+    for i in range(steps):
+        step(i, evs.get(i))
+    stop.record(st)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__(None, None, None)
+    _barrier(world)
+    ms = _max_over_ranks(start.elapsed_time(stop), dev, world) / steps
     k1_ms = statistics.mean(a.elapsed_time(c) for a, c in evs.values())
     stats = canny.read_stats(ws)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms = total_ms / args.steps
-    value = world * px / 1e6 / (ms / 1e3)
+    out = {"ms": ms, "k1_ms": k1_ms, "k1_samples": len(evs), "ev_every": EV_EVERY, "stats": stats, "nbuf": nbuf,
+           "clocks": clk.summary() if clk else None, "px": px}
+    del srcs, labels, final, ws
+    torch.cuda.empty_cache()
+    return out
 
-    # e2e: host buffers through the C ABI (pinned), copies inside the timed region
+
+def measure_e2e(frames, weights, low, high, steps, dev, world):
+    """ef_canny_u8_host: pinned host input -> host labels/final, copies inside the timed region."""
+    import torch
+
+    from paper_1710_07745_b200 import canny
+
+    b, h, wd = frames.shape
+    px = frames.size
+    hsrc = torch.from_numpy(frames).pin_memory()
+    hlab = torch.empty_like(hsrc).pin_memory()
+    hfin = torch.empty_like(hsrc).pin_memory()
+    for _ in range(2):
+        canny.canny_u8_host_ptr(hsrc.data_ptr(), b, h, wd, weights, low, high, hlab.data_ptr(), hfin.data_ptr(),
+                                dev.index)
+    _barrier(world)
+    e_steps = max(3, min(steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        canny.canny_u8_host_ptr(hsrc.data_ptr(), b, h, wd, weights, low, high, hlab.data_ptr(), hfin.data_ptr(),
+                                dev.index)
+    e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+    e_ms = _max_over_ranks(e_ms, dev, world)
+    return e_ms, e_steps
+
+
+def measure_bands(frame_rank0, weights, low, high, steps, warmup, dev, rank, world, peer=False):
+    """C4: one frame in row bands, one band per rank; the frame is generated on
+    rank 0 and broadcast once (setup, untimed).  Returns ms per frame (max over ranks)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_07745_b200 import bands
+
+    if world > 1:
+        hw = torch.tensor(list(frame_rank0.shape) if rank == 0 else [0, 0], dtype=torch.int64, device=dev)
+        dist.broadcast(hw, 0)
+        H, W = (int(v) for v in hw.tolist())
+        full = (torch.from_numpy(frame_rank0).to(dev) if rank == 0
+                else torch.empty((H, W), dtype=torch.uint8, device=dev))
+        dist.broadcast(full, 0)
+    else:
+        H, W = frame_rank0.shape
+        full = torch.from_numpy(np.ascontiguousarray(frame_rank0)).to(dev)
+    r = (len(weights) - 1) // 2
+    s0, s1 = bands.band_plan(H, world)[rank]
+    staged, band = bands.band_buffer(s1 - s0, W, s0, H, r, device=dev)
+    band.copy_(full[s0:s1])  # halo rows arrive in place each step
+    del full
+    st = torch.cuda.current_stream()
+    be = bands.CudaBandBackend(s1 - s0, W)  # workspace and band metadata reused across steps
+
+    def step():
+        bands.distributed_band_canny(band, s0, H, weights, low, high, backend=be,
+                                     staged=None if peer else staged, peer=peer)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(st)
+    for _ in range(steps):
+        step()
+    stop.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = _max_over_ranks(start.elapsed_time(stop), dev, world) / steps
+    if peer:
+        be.close_peers()
+    del staged, band, be
+    torch.cuda.empty_cache()
+    return ms, H, W
+
+
+def _init_dist(world, local):
+    """NCCL process group (also a 1-rank group for the band path at N=1)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    return dev
+
+
+def _ensure_group(dev):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{_free_port()}",
+                                device_id=dev)
+
+
+def run_bands(args):
+    """Config 4 across ranks: one 16384^2 frame, row bands (one per GPU), halo
+    rows and band-edge component ids exchanged over NCCL (bands.py).  Total
+    work is fixed as N grows: "scaling": "strong"."""
+    from paper_1710_07745_b200 import synth
+    from paper_1710_07745_b200.filtering import build_gaussian_kernel
+
+    rank, world, local = dist_env()
+    frame = None
+    if rank == 0:
+        frame = synth.config4() if not args.frames else synth.config4(args.frames * 1024, tile=256)
+    dev = _init_dist(world, local)
+    _ensure_group(dev)
+    low, high = synth.CONFIG_THRESHOLDS[4]
+    w = build_gaussian_kernel(1.4, radius=args.radius).weights
+    ms, H, W = measure_bands(frame, w, low, high, args.steps, args.warmup, dev, rank, world, peer=args.peer)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(H * W / 1e6 / (ms / 1e3), 3), "unit": "MP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
+                "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
+                "config": {"workload": f"C4: one {H}x{W} frame, row bands over {world} GPU(s)",
+                           "radius": args.radius, "thresholds": [low, high],
+                           "parallelism": f"{world} row bands, " + ("halo rows read in place from peer HBM (CUDA IPC)"
+                                                                      if args.peer else "NCCL P2P halo exchange")
+                                          + ", all_gather of edge ids, device seam merge"},
+                "e2e": None, "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
+
+
+def run_ours(args):
+    import torch
+
+    from paper_1710_07745_b200 import synth
+    from paper_1710_07745_b200.filtering import build_gaussian_kernel
+
+    rank, world, local = dist_env()
+    # host-side inputs first (forked generator workers, before any CUDA state)
+    frames, name, low, high, n_total = workload(args.config, args.frames, rank, world)
+    extra = not args.no_extra and args.config == 3
+    c1 = workload(1, None, rank, world) if extra else None
+    c4 = synth.config4() if (extra and rank == 0) else None
+    dev = _init_dist(world, local)
+    w = build_gaussian_kernel(1.4, radius=args.radius).weights
+    b, h, wd = frames.shape
+    px = frames.size
+
+    m = measure_batch(frames, w, low, high, args.steps, args.warmup, dev, world)
+    ms = m["ms"]
+    total_px = n_total * h * wd
+    value = total_px / 1e6 / (ms / 1e3)
+
     e2e = None
     if not args.no_e2e:
-        hsrc = torch.from_numpy(frames).pin_memory()
-        hlab = torch.empty_like(hsrc).pin_memory()
-        hfin = torch.empty_like(hsrc).pin_memory()
-        for _ in range(2):
-            canny.canny_u8_host_ptr(hsrc.data_ptr(), b, h, wd, w, low, high, hlab.data_ptr(), hfin.data_ptr(),
-                                    dev.index)
-        if world > 1:
-            torch.distributed.barrier()
-        e_steps = max(3, min(args.steps, 10))
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            canny.canny_u8_host_ptr(hsrc.data_ptr(), b, h, wd, w, low, high, hlab.data_ptr(), hfin.data_ptr(),
-                                    dev.index)
-        e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
-        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(et.item())
-        e2e = {"value": round(world * px / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s", "ms_per_step": round(e_ms, 3),
-               "h2d_bytes_per_step": int(px), "d2h_bytes_per_step": int(-(-px // 4)),
-               "path": "ef_canny_u8_host (pinned input; 3-stream chunked copy/compute overlap; labels+final "
-                       "cross PCIe packed to 2 bits/px and are expanded into the host arrays by a host thread pool)"}
+        e_ms, e_steps = measure_e2e(frames, w, low, high, args.steps, dev, world)
+        e2e = {"value": round(total_px / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s", "ms_per_step": round(e_ms, 3),
+               "steps": e_steps, "h2d_bytes_per_step": int(total_px), "d2h_bytes_per_step": int(world * -(-px // 4)),
+               "path": "ef_canny_u8_host per rank (pinned input; 3-stream chunked copy/compute overlap; labels+final "
+                       "cross PCIe packed to 2 bits/px and are expanded into the host arrays by a host thread pool); "
+                       "wall clock, max over ranks"}
+
+    extras = {}
+    if extra:
+        f1, n1, lo1, hi1, tot1 = c1
+        m1 = measure_batch(f1, w, lo1, hi1, args.steps, args.warmup, dev, world, sample_clocks=False)
+        extras["c1"] = {"workload": n1 + f", sharded {tot1}/{world}", "value": round(
+            tot1 * 1080 * 1920 / 1e6 / (m1["ms"] / 1e3), 3), "unit": "MP/s", "ms_per_step": round(m1["ms"], 4),
+            "k1_ms": round(m1["k1_ms"], 4), "k1_frac_3bpx": round(
+                3 * f1.size / (m1["k1_ms"] / 1e3) / 1e9 / peaks()[0], 4), "fixups": m1["stats"]["fixups"]}
+        del f1
+        try:
+            _ensure_group(dev)
+            lo4, hi4 = synth.CONFIG_THRESHOLDS[4]
+            ms4, H4, W4 = measure_bands(c4, w, lo4, hi4, max(5, args.steps // 2), 2, dev, rank, world)
+            extras["c4_bands"] = {"workload": f"C4: one {H4}x{W4} frame, {world} row band(s), one per GPU "
+                                              f"(NCCL halo exchange, all_gather of edge ids, device seam merge)",
+                                  "value": round(H4 * W4 / 1e6 / (ms4 / 1e3), 3), "unit": "MP/s",
+                                  "ms_per_step": round(ms4, 4), "scaling": "strong"}
+        except Exception as exc:  # noqa: BLE001  (a secondary number must not hide the headline)
+            extras["c4_bands"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     peak, peak_kind = peaks()
     # algorithmic bytes of the roofline kernel: u8 in + label byte out (SURVEY 8d's
     # 2 B/px) + the final byte the fused K1 also writes (final = strong; the
     # hysteresis only adds the weak pixels that join an edge) = 3 B/px
     alg_bytes = 3 * px
+    k1_ms = m["k1_ms"]
     achieved = alg_bytes / (k1_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.config, n_total if world == 1 else -1, args.radius)
     if rank == 0:
         # the CPU baseline is timed on rank 0 at N=1 only (a reported baseline, not per-rank work)
         cpu = None if (args.no_cpu or world > 1) else cpu_baseline(frames, w, low, high)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong" if args.config in (1, 3) else "replicas",
+            "vs_baseline": None, "dtype": "f32",
+            "dtype_note": "certified f32 decisions, f64 fix-up of uncertified pixels; u8 in, u8 out",
             "data": "synthetic (seeded generators, paper_1710_07745_b200/synth.py)",
-            "config": {"workload": name, "frames_per_gpu": int(b), "height": int(h), "width": int(wd),
-                       "radius": args.radius, "sigma": 1.4, "thresholds": [low, high],
-                       "parallelism": f"{world} independent batches (one per GPU)",
-                       "l2": f"rotating {nbuf} resident input batches ({nbuf * px / 1e6:.0f} MB > 126 MB L2)"},
+            "config": {"workload": name, "frames_total": int(n_total), "frames_per_gpu": int(b), "height": int(h),
+                       "width": int(wd), "radius": args.radius, "sigma": 1.4, "thresholds": [low, high],
+                       "parallelism": f"dp{world}: {n_total} frames sharded {n_total}/{world} per GPU, "
+                                      f"no data-path collective",
+                       "l2": (f"input batch {px / 1e6:.0f} MB per GPU > 126 MB L2 (no rotation needed)" if m["nbuf"] == 1
+                              else f"rotating {m['nbuf']} resident input batches ({m['nbuf'] * px / 1e6:.0f} MB > "
+                                   f"126 MB L2)")},
             "roofline": {"bound": "hbm", "kernel": "k1v3_kernel (+fix-up launches)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic() if (args.config == 1 and b == 64 and args.radius == 2) else None,
-                         "traffic_source": "profiles/r01_k1v3_dram_64frames.csv (ncu dram__bytes_read+write per launch)",
+                         "traffic": traffic,
+                         "traffic_source": (f"{traffic_src} (ncu dram__bytes_read+write per K1 launch)"
+                                            if traffic_src else None),
                          "peak_kind": peak_kind,
                          "alg_bytes_per_launch": int(alg_bytes),
                          "alg_bytes_note": "3 B/px: u8 in, label out, final out (K1 writes final = strong in the "
@@ -418,21 +581,30 @@ def run_ours(args):
                          "frac_at_2bpx": round(achieved * 2 / 3 / peak, 4),
                          "avg_launch_ms": round(k1_ms, 4),
                          "timing": f"CUDA events the library records on the launching stream around K1 + fix-ups, "
-                                   f"on {len(evs)} of the {args.steps} timed steps (every {EV_EVERY}th)",
+                                   f"on {m['k1_samples']} of the {args.steps} timed steps (every {m['ev_every']}th), "
+                                   f"rank 0",
                          "share_of_step": round(k1_ms / ms, 3)},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": m["clocks"],
             "gpu_launches": 8 * args.steps,  # ws_begin, K1, fix-up, H1, dense H1, merge, resolve, finalize
-            "stats": {k: int(v) for k, v in stats.items()},
+            "stats": {k: int(v) for k, v in m["stats"].items()},
+            "extra": extras or None,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    rank, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     elif args.bands:

@@ -125,3 +125,22 @@ def trace(labels: np.ndarray) -> np.ndarray:
 
 def quantize(gx: float, gy: float) -> int:
     return int(_load().ef_oracle_quantize(float(gx), float(gy)))
+
+
+def blur(pixels: np.ndarray, weights: np.ndarray) -> np.ndarray:
+    """gaussian_blur (filtering.py:43-91) for one float64 frame: the oracle's C
+    restatement's `blurred` stage."""
+    return stages(pixels, weights, 0.0, 0.0)["blurred"]
+
+
+def laplacian(blurred: np.ndarray) -> np.ndarray:
+    """Restates laplacian (gradient.py:93-107) over _stencil_band
+    (gradient.py:51-70): replicate 1-pixel margin, LAPLACIAN_MASK taps in
+    row-major order, zero taps skipped, accumulated from +0.0 with separately
+    rounded multiply and add (numpy elementwise float64 ops, no FMA)."""
+    p = np.pad(np.asarray(blurred, dtype=np.float64), 1, mode="edge")
+    h, w = p.shape[0] - 2, p.shape[1] - 2
+    out = np.zeros((h, w), np.float64)
+    for dy, dx, c in ((0, 1, 1.0), (1, 0, 1.0), (1, 1, -4.0), (1, 2, 1.0), (2, 1, 1.0)):
+        out = out + c * p[dy:dy + h, dx:dx + w]
+    return out

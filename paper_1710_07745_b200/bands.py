@@ -44,6 +44,20 @@ def band_plan(height: int, nbands: int) -> list[tuple[int, int]]:
     return [(s, min(s + size, height)) for s in range(0, height, size)]
 
 
+def check_band_meta(meta: list[tuple[int, int]], full_height: int) -> None:
+    """The seam merge joins gathered block k's bottom row to block k+1's top
+    row, so rank k must hold the k-th band from the top: bands sorted by row0 in
+    rank order, contiguous, covering [0, full_height)."""
+    row = 0
+    for rank, (r0, rows) in enumerate(meta):
+        if r0 != row or rows < 1:
+            raise ValueError(f"row bands must be contiguous, non-empty and in rank order from row 0: rank {rank} "
+                             f"holds rows [{r0}, {r0 + rows}), expected to start at row {row}")
+        row = r0 + rows
+    if row != full_height:
+        raise ValueError(f"row bands cover rows [0, {row}) of a {full_height}-row frame")
+
+
 def halo_rows(radius: int) -> int:
     return radius + 2  # blur radius + Sobel 1 + NMS 1 (ef_band_halo_rows)
 
@@ -330,6 +344,7 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     else:
         counts = _gather(torch.tensor([row0, rows], dtype=torch.int64, device=band_u8.device), world, group)
         meta = [(int(c[0]), int(c[1])) for c in counts]
+        check_band_meta(meta, full_height)
         be.band_meta = (key, meta)
     ht = min(halo, row0)
     hb = min(halo, full_height - row0 - rows)

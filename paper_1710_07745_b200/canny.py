@@ -16,8 +16,7 @@ import numpy as np
 
 from . import _lib
 
-_ws_lock = threading.Lock()
-_ws_cache: dict[int, "object"] = {}
+_ws_local = threading.local()
 
 
 def _torch():
@@ -56,16 +55,29 @@ def host_weights(weights) -> tuple[np.ndarray, ctypes.c_void_p, int]:
     return w, w.ctypes.data_as(ctypes.c_void_p), r
 
 
-def workspace(batch: int, height: int, width: int, device=None):
-    """A cached device workspace large enough for (batch, height, width)."""
+def workspace(batch: int, height: int, width: int, device=None, stream=None):
+    """A cached device workspace large enough for (batch, height, width).
+
+    One cache per (host thread, device, stream): the header's thread-safety rule
+    is one workspace per concurrent launch sequence, and two threads (or two
+    streams) sharing one would reset each other's counters and bit planes
+    mid-call.  The tensor is marked in use on the launch stream, so a workspace
+    that is replaced (grown) is not recycled while queued kernels still use it."""
     torch = require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
     need = int(_lib.load().ef_workspace_bytes(batch, height, width))
-    with _ws_lock:
-        ws = _ws_cache.get(dev.index)
-        if ws is None or ws.numel() < need:
+    cache = getattr(_ws_local, "cache", None)
+    if cache is None:
+        cache = _ws_local.cache = {}
+    key = (dev.index, int(st.cuda_stream))
+    ws = cache.get(key)
+    if ws is None or ws.numel() < need:
+        if ws is not None:
+            ws.record_stream(st)  # freed only after the work already queued on `st`
+        with torch.cuda.stream(st):  # allocated on the launch stream's pool
             ws = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
-            _ws_cache[dev.index] = ws
+        cache[key] = ws
     return ws
 
 
@@ -94,7 +106,7 @@ def canny_u8(frames, weights, low: float, high: float, labels=None, final=None, 
     b, h, w = x.shape
     labels = torch.empty_like(x) if labels is None else labels
     final = torch.empty_like(x) if final is None else final
-    ws = workspace(b, h, w) if ws is None else ws
+    ws = workspace(b, h, w, x.device, stream) if ws is None else ws
     _, wp, r = host_weights(weights)
     rc = _lib.load().ef_canny_u8(_ptr(x), b, h, w, wp, r, float(low), float(high), _ptr(labels), _ptr(final),
                                  _ptr(ws), ws.numel(), _stream_ptr(stream))
@@ -107,7 +119,7 @@ def classify_u8(frames, weights, low: float, high: float, labels=None, ws=None, 
     x = _frames(frames, "torch.uint8")
     b, h, w = x.shape
     labels = torch.empty_like(x) if labels is None else labels
-    ws = workspace(b, h, w) if ws is None else ws
+    ws = workspace(b, h, w, x.device, stream) if ws is None else ws
     _, wp, r = host_weights(weights)
     rc = _lib.load().ef_classify_u8(_ptr(x), b, h, w, wp, r, float(low), float(high), _ptr(labels), _ptr(ws),
                                     ws.numel(), _stream_ptr(stream))
@@ -121,7 +133,7 @@ def canny_f64(frames, weights, low: float, high: float, ws=None, stream=None):
     b, h, w = x.shape
     labels = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
     final = torch.empty_like(labels)
-    ws = workspace(b, h, w) if ws is None else ws
+    ws = workspace(b, h, w, x.device, stream) if ws is None else ws
     _, wp, r = host_weights(weights)
     rc = _lib.load().ef_canny_f64(_ptr(x), b, h, w, wp, r, float(low), float(high), _ptr(labels), _ptr(final),
                                   _ptr(ws), ws.numel(), _stream_ptr(stream))
@@ -134,7 +146,7 @@ def trace_edges_u8(labels, final=None, ws=None, stream=None):
     x = _frames(labels, "torch.uint8")
     b, h, w = x.shape
     final = torch.empty_like(x) if final is None else final
-    ws = workspace(b, h, w) if ws is None else ws
+    ws = workspace(b, h, w, x.device, stream) if ws is None else ws
     rc = _lib.load().ef_trace_edges(_ptr(x), b, h, w, _ptr(final), _ptr(ws), ws.numel(), _stream_ptr(stream))
     _lib.check(rc, "ef_trace_edges")
     return final

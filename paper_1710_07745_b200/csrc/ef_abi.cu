@@ -197,6 +197,26 @@ int check_dims(int64_t batch, int32_t H, int32_t W) {
     return EF_OK;
 }
 
+// numpy's float64 add.reduce of a short contiguous vector (its pairwise
+// summation below the 128-element block: eight interleaved partial sums, a
+// fixed combine tree, then the tail), so weights on the 1e-12 edge are
+// accepted or rejected exactly as GaussianKernel's w.sum() does.
+double numpy_sum(const double* a, int n) {
+    if (n < 8) {
+        double s = -0.0;
+        for (int i = 0; i < n; ++i) s += a[i];
+        return s;
+    }
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) s += a[i];
+    return s;
+}
+
 // GaussianKernel validation (filtering.py:20-29) plus the threshold validation
 // (hysteresis.py:31-33).
 int check_params(const double* w, int32_t r, double low, double high) {
@@ -204,13 +224,13 @@ int check_params(const double* w, int32_t r, double low, double high) {
     if (r < 0 || r > EF_MAX_RADIUS)
         return fail(EF_EINVAL, "radius must be in [0, " + std::to_string(EF_MAX_RADIUS) + "], got " +
                                    std::to_string(r));
-    double sum = 0.0;
     for (int i = 0; i <= 2 * r; ++i) {
         if (!std::isfinite(w[i])) return fail(EF_EINVAL, "kernel weights must be finite");
         if (w[i] != w[2 * r - i]) return fail(EF_EINVAL, "kernel weights must be symmetric");
-        sum += w[i];
     }
-    if (std::fabs(sum - 1.0) > 1e-9) return fail(EF_EINVAL, "kernel weights must sum to 1");
+    const double sum = numpy_sum(w, 2 * r + 1);
+    // GaussianKernel's own check (filtering.py:25-26): |sum - 1| <= 1e-12
+    if (!(std::fabs(sum - 1.0) <= 1e-12)) return fail(EF_EINVAL, "kernel weights must sum to 1");
     if (!(0.0 <= low && low <= high))
         return fail(EF_EINVAL, "need 0 <= low <= high, got low=" + std::to_string(low) +
                                    ", high=" + std::to_string(high));
@@ -270,6 +290,8 @@ Timing& timing() {
     return t;
 }
 
+bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) == 0; }
+
 bool has_negative(const double* w, int r) {
     for (int i = 0; i <= 2 * r; ++i)
         if (w[i] < 0.0) return true;
@@ -296,6 +318,10 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
         return EF_OK;
     }
     FastParams FP = make_fast(w, r, low, high);
+    // the production classifier moves 32-bit words: misaligned caller buffers
+    // take the byte-wise generic classifier (g.top/g.bot peer rows are checked
+    // by the peer entry point)
+    FP.no_v2 = !aligned4(src) || !aligned4(labels) || (fin && !aligned4(fin));
     FgBits B{};
     unsigned long long nwords = 0;  // bit-plane words ws_begin zeroes (both planes and the gap between)
     static const bool no_bits = getenv("EF_NO_FG_BITS") != nullptr;  // A/B switch for profiling
@@ -330,6 +356,8 @@ int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, 
 
 int check_ws(void* ws, size_t bytes, const WsLayout& L) {
     if (!ws) return fail(EF_EINVAL, "workspace pointer is NULL");
+    if (reinterpret_cast<uintptr_t>(ws) % kAlign)
+        return fail(EF_EINVAL, "workspace must be 256-byte aligned (cudaMalloc / torch allocations are)");
     if (bytes < L.total)
         return fail(EF_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes, got " +
                                    std::to_string(bytes));
@@ -850,6 +878,9 @@ int ef_band_canny_u8_peer(const uint8_t* d_band, const uint8_t* d_top, int32_t t
                                "min(full_height-row0-rows, radius+2) rows below the band");
     FastParams FP = make_fast(h_weights, radius, low, high);
     if (has_negative(h_weights, radius)) return fail(EF_EINVAL, "signed kernel on a band");
+    if (!aligned4(d_band) || !aligned4(d_labels) || !aligned4(d_final) || (ht && !aligned4(d_top)) ||
+        (hb && !aligned4(d_bot)))
+        return fail(EF_EINVAL, "peer halos need 4-byte aligned band, halo, labels and final buffers");
     FrameGeom g{ht + rows + hb, width, row0 - ht, full_height, row0, rows};
     g.top = ht > 0 ? d_top : nullptr;
     g.bot = hb > 0 ? d_bot : nullptr;

@@ -37,6 +37,7 @@ struct FastParams {
     float e_nms;  // |c - n| > e_nms -> the NMS comparison is certain
     float e_sec;  // |t*a - b| > e_sec -> the orientation sector is certain
     int cls0;     // class of a suppressed pixel (thinned value 0.0)
+    int no_v2;    // a caller buffer is not 4-byte aligned: the generic byte-wise classifier only
 };
 
 // Workspace header (device memory, start of the caller's workspace).

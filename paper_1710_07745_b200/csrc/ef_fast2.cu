@@ -602,7 +602,11 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
 
-bool k1v2_supported(const FastParams& P, const FrameGeom& g) { return P.r >= 1 && P.r <= 6 && (g.W % 4) == 0; }
+// the production classifier reads the source and writes labels / final in
+// 32-bit words: every caller buffer 4-byte aligned (P.no_v2 == 0), W % 4 == 0
+bool k1v2_supported(const FastParams& P, const FrameGeom& g) {
+    return !P.no_v2 && P.r >= 1 && P.r <= 6 && (g.W % 4) == 0;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {

@@ -11,9 +11,14 @@
 //     arrays with non-temporal stores (no read-for-ownership, pageable or not);
 //   * pageable inputs are staged into pinned memory by the same pool, so the
 //     DMA always runs from pinned pages.
+#if defined(__x86_64__) && !defined(EF_PORTABLE_HOST)
+#define EF_X86 1
 #include <emmintrin.h>
 #include <immintrin.h>
 #include <cpuid.h>
+#else
+#define EF_X86 0  // aarch64 (Grace): scalar unpack, plain copies, no cache-line eviction
+#endif
 #include <sched.h>
 
 #include <algorithm>
@@ -97,6 +102,7 @@ const Luts& luts() {
 
 // Evict the packed staging lines after the unpack has read them: the next
 // D2H into lines still held by the CPU caches runs several times slower.
+#if EF_X86
 __attribute__((target("clflushopt"))) static void flush_opt(const uint8_t* p, size_t n) {
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(63);
     for (uintptr_t a = a0; a < reinterpret_cast<uintptr_t>(p) + n; a += 64) _mm_clflushopt((void*)a);
@@ -116,7 +122,11 @@ void flush_lines(const uint8_t* p, size_t n) {
     for (uintptr_t a = a0; a < reinterpret_cast<uintptr_t>(p) + n; a += 64) _mm_clflush((void*)a);
     _mm_mfence();
 }
+#else
+void flush_lines(const uint8_t*, size_t) {}  // coherent DMA; eviction is an x86 tuning only
+#endif
 
+#if EF_X86
 // AVX2 + BMI2 body: 8 packed bytes (32 pixels) per step.  pdep spreads each
 // 2-bit code into a byte; label = (code + 1) >> 1 and final = code >> 1 bytewise
 // (codes <= 3, so no carries cross bytes); two 32-byte non-temporal stores.
@@ -144,6 +154,7 @@ static bool has_avx2_bmi2() {
     static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("bmi2");
     return ok;
 }
+#endif
 
 void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx, uint8_t* labels,
                   uint8_t* final_map) {
@@ -156,6 +167,7 @@ void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx,
         std::memcpy(labels + 4 * b, &l, 4);
         std::memcpy(final_map + 4 * b, &f, 4);
     };
+#if EF_X86
     const bool same_phase32 = ((reinterpret_cast<uintptr_t>(labels) ^ reinterpret_cast<uintptr_t>(final_map)) & 31) == 0;
     if (same_phase32 && has_avx2_bmi2()) {
         while (j < full_end && (reinterpret_cast<uintptr_t>(labels + 4 * j) & 31)) scalar(j++);
@@ -174,6 +186,7 @@ void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx,
         }
         _mm_sfence();
     }
+#endif
     for (; j < full_end; ++j) scalar(j);
     if (j < byte1 && 4 * j < npx) {  // last partial byte
         const uint32_t l = T.lab[packed[j]], f = T.fin[packed[j]];
@@ -249,6 +262,10 @@ void Latch::wait() {
 // copy into pinned staging with non-temporal stores: the DMA that reads the
 // staging next must not find its lines dirty in the CPU caches
 static void stream_copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
+#if !EF_X86
+    std::memcpy(dst, src, bytes);
+    return;
+#else
     size_t i = 0;
     while (i < bytes && (reinterpret_cast<uintptr_t>(dst + i) & 15)) {
         dst[i] = src[i];
@@ -266,6 +283,7 @@ static void stream_copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
     }
     _mm_sfence();
     for (; i < bytes; ++i) dst[i] = src[i];
+#endif
 }
 
 static bool f64_to_u8(const double* src, size_t n, uint8_t* dst) {

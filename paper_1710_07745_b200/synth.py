@@ -157,8 +157,9 @@ def config1_frame(index: int, height: int = 1080, width: int = 1920, base_seed: 
     return _finish(canvas, rng, 5.0)
 
 
-def config1(frames: int = 64, height: int = 1080, width: int = 1920) -> np.ndarray:
-    return np.stack([config1_frame(i, height, width) for i in range(frames)])
+def config1(frames: int = 64, height: int = 1080, width: int = 1920, workers: int | None = None) -> np.ndarray:
+    out = np.empty((frames, height, width), dtype=np.uint8)
+    return _fill_parallel(out, lambda i: config1_frame(i, height, width), workers)
 
 
 def config2(size: int = 4096, seed: int = 2) -> np.ndarray:
@@ -179,12 +180,12 @@ def _value_noise(rng, h, w, octaves=4, amplitude=60.0):
         ty, tx = fy - iy, fx - ix
         ty = ty * ty * (3.0 - 2.0 * ty)
         tx = tx * tx * (3.0 - 2.0 * tx)
-        a = lat[iy][:, ix]
-        b = lat[iy][:, ix + 1]
-        c = lat[iy + 1][:, ix]
-        d = lat[iy + 1][:, ix + 1]
-        top = a + (b - a) * tx[None, :]
-        bot = c + (d - c) * tx[None, :]
+        # x-interpolate each lattice row once, then pick rows per image row: the
+        # same operations on the same operands as a per-pixel 2-D gather
+        la, lb = lat[:, ix], lat[:, ix + 1]
+        rows = la + (lb - la) * tx[None, :]
+        top = rows[iy]
+        bot = rows[iy + 1]
         out += amp * (top + (bot - top) * ty[:, None])
         total += amp
         amp *= 0.5
@@ -201,8 +202,47 @@ def config3_image(index: int, size: int = 1024, base_seed: int = 3000) -> np.nda
     return _finish(canvas, rng, 8.0)
 
 
-def config3(images: int = 1024, size: int = 1024) -> np.ndarray:
-    return np.stack([config3_image(i, size) for i in range(images)])
+def _fill_parallel(out: np.ndarray, make, workers: int | None = None) -> np.ndarray:
+    """out[i] = make(i) for every i, in forked worker processes writing into a
+    shared anonymous mapping (each image depends only on its own seed, so the
+    bytes equal the serial loop's)."""
+    import mmap
+    import multiprocessing as mp
+    import os
+
+    n = len(out)
+    workers = workers or min(n, len(os.sched_getaffinity(0)))
+    if workers <= 1 or n < 8 or "fork" not in mp.get_all_start_methods():
+        for i in range(n):
+            out[i] = make(i)
+        return out
+    buf = mmap.mmap(-1, out.nbytes)
+    shared = np.frombuffer(buf, dtype=out.dtype).reshape(out.shape)
+    chunks = [range(k, n, workers) for k in range(workers)]
+    pids = []
+    for ch in chunks:
+        pid = os.fork()
+        if pid == 0:  # child: numpy only, no CUDA
+            code = 0
+            try:
+                for i in ch:
+                    shared[i] = make(i)
+            except BaseException:  # noqa: BLE001
+                code = 1
+            os._exit(code)
+        pids.append(pid)
+    bad = [pid for pid in pids if os.waitpid(pid, 0)[1] != 0]
+    if bad:
+        raise RuntimeError(f"synthetic image workers failed: {bad}")
+    out[...] = shared
+    del shared
+    buf.close()
+    return out
+
+
+def config3(images: int = 1024, size: int = 1024, workers: int | None = None) -> np.ndarray:
+    out = np.empty((images, size, size), dtype=np.uint8)
+    return _fill_parallel(out, lambda i: config3_image(i, size), workers)
 
 
 def config4(size: int = 16384, seed: int = 4, tile: int = 2048) -> np.ndarray:
@@ -250,3 +290,15 @@ def make_config(cfg: int, reduced: bool = False) -> np.ndarray:
     if cfg == 4:
         return config4(1024, tile=256)[None] if reduced else config4()[None]
     raise ValueError(f"unknown config {cfg}")
+
+
+def config_range(cfg: int, lo: int, hi: int, workers: int | None = None) -> np.ndarray:
+    """Frames [lo, hi) of batched config 1 or 3 (a rank's shard): equal to
+    make_config(cfg)[lo:hi], generated without the other frames."""
+    if cfg == 1:
+        out = np.empty((hi - lo, 1080, 1920), dtype=np.uint8)
+        return _fill_parallel(out, lambda i: config1_frame(lo + i), workers)
+    if cfg == 3:
+        out = np.empty((hi - lo, 1024, 1024), dtype=np.uint8)
+        return _fill_parallel(out, lambda i: config3_image(lo + i), workers)
+    raise ValueError(f"config {cfg} is not a batch")

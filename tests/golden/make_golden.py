@@ -18,6 +18,11 @@ Fixtures:
                 the reference default radius 5; inputs are pinned by sha256.
   quantize.npz  quantize_orientation on axis, diagonal and near-boundary
                 gradient pairs.
+  laplacian.npz run_pipeline(operator="laplacian", keep_intermediates=True)
+                response + blurred for the fixture set (sigma 1.4 and 0.6), and
+                gaussian_blur -> laplacian with the configs' radius-2 kernel.
+
+    python tests/golden/make_golden.py [stages pipeline configs quantize laplacian]
 """
 
 from __future__ import annotations
@@ -103,7 +108,37 @@ def pack(b):
     return np.packbits(np.asarray(b, dtype=bool).ravel())
 
 
+def make_laplacian():
+    out = {}
+    names = []
+    cases = [c for c in fixture_set() if not c[0].startswith(("c0_", "c2_"))]
+    rng = np.random.default_rng(4242)
+    cases.append(("u8_40x50", rng.integers(0, 256, (40, 50)).astype(np.float64)))
+    cases.append(("c3_crop_48", synth.config3_image(0)[200:248, 300:348].astype(np.float64)))
+    for name, arr in cases:
+        img = ef.GrayImage.from_array(arr)
+        names.append(name)
+        out[f"{name}/input"] = arr
+        for sigma in (1.4, 0.6):
+            res = ef.run_pipeline(img, ef.PipelineConfig(sigma=sigma, operator="laplacian"), keep_intermediates=True)
+            out[f"{name}/s{sigma}/response"] = res.response.pixels
+            out[f"{name}/s{sigma}/blurred"] = res.blurred.pixels
+            out[f"{name}/s{sigma}/weights"] = ef.build_gaussian_kernel(sigma).weights.copy()
+        k = kernel(1.4, 2)
+        blurred = ef.gaussian_blur(img, k, W1)
+        out[f"{name}/r2/response"] = ef.gradient.laplacian(blurred, W1).pixels
+        out[f"{name}/r2/weights"] = k.weights.copy()
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "laplacian.npz"), **out)
+    print("laplacian.npz", os.path.getsize(os.path.join(HERE, "laplacian.npz")))
+
+
 def main():
+    which = set(sys.argv[1:]) or {"stages", "pipeline", "configs", "quantize", "laplacian"}
+    if "laplacian" in which:
+        make_laplacian()
+    if which <= {"laplacian"}:
+        return
     out = {}
     # ---------------- stages ----------------
     rng = np.random.default_rng(77)

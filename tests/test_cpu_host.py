@@ -190,3 +190,70 @@ def test_host_f64_to_u8_integer_test():
         b[rng.integers(0, 517), rng.integers(0, 1031)] = bad
         assert ef.GrayImage.from_array(b).as_u8() is None, bad
     assert ef.GrayImage.from_array(np.zeros((3, 5))).as_u8() is not None
+
+
+def _canny_u8_call(weights, ws_ptr=None, ws_bytes=1 << 30):
+    """ef_canny_u8 with dummy device pointers: argument validation runs on the
+    host before anything touches a device, so the status and message are
+    observable without a GPU."""
+    lib = _lib.load()
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    r = (len(w) - 1) // 2
+    rc = lib.ef_canny_u8(0x1000, 1, 8, 8, w.ctypes.data, r, 20.0, 50.0, 0x2000, 0x3000, ws_ptr, ws_bytes, None)
+    return rc, lib.ef_last_error().decode()
+
+
+def test_abi_weight_sum_tolerance_matches_gaussian_kernel():
+    """check_params mirrors GaussianKernel (filtering.py:25-26): |sum - 1| <= 1e-12
+    with numpy's summation order; beyond it EF_EINVAL (ValueError)."""
+    good = ef.build_gaussian_kernel(1.4, radius=5).weights
+    rc, msg = _canny_u8_call(good)  # valid weights: fails later, on the NULL workspace
+    assert rc == _lib.EF_EINVAL and "workspace" in msg
+    for eps in (3e-12, 1e-10, 1e-9 / 2):
+        bad = np.array(good, copy=True)
+        bad[5] += eps
+        rc, msg = _canny_u8_call(bad)
+        assert rc == _lib.EF_EINVAL and "sum to 1" in msg, eps
+        with pytest.raises(ValueError):
+            ef.GaussianKernel(sigma=1.4, radius=5, weights=bad)
+    # accepted / rejected exactly where the Python mirror (numpy sum) says so
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        r = int(rng.integers(0, 16))
+        half = rng.random(r + 1) + 0.1
+        w = np.concatenate([half[:0:-1], half]) if r else half[:1]
+        w = w / w.sum()
+        w = w + (rng.integers(-3, 4) * 2e-13 if rng.random() < 0.5 else 0.0)
+        w = (w + w[::-1]) / 2.0
+        ok = abs(w.sum() - 1.0) <= 1e-12
+        rc, msg = _canny_u8_call(w)
+        assert ("sum to 1" not in msg) == ok, (r, w.sum() - 1.0)
+
+
+def test_abi_rejects_misaligned_workspace():
+    w = ef.build_gaussian_kernel(1.4, radius=2).weights
+    rc, msg = _canny_u8_call(w, ws_ptr=0x100010)
+    assert rc == _lib.EF_EINVAL and "256-byte aligned" in msg
+
+
+def test_portable_host_build_compiles():
+    """ef_host.cu builds without the x86 intrinsics (aarch64 / Grace hosts):
+    the portable branch, forced with -DEF_PORTABLE_HOST."""
+    import subprocess
+    import tempfile
+
+    from paper_1710_07745_b200 import build as B
+
+    with tempfile.TemporaryDirectory() as d:
+        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, "-DEF_PORTABLE_HOST", "-c", os.path.join(B.CSRC, "ef_host.cu"), "-o",
+               os.path.join(d, "h.o")]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr
+
+
+def test_band_meta_must_be_contiguous_in_rank_order():
+    bands.check_band_meta([(0, 10), (10, 5), (15, 1)], 16)
+    for meta, h in (([(10, 6), (0, 10)], 16), ([(0, 10), (11, 5)], 16), ([(0, 10), (10, 5)], 16),
+                    ([(0, 0), (0, 16)], 16)):
+        with pytest.raises(ValueError):
+            bands.check_band_meta(meta, h)

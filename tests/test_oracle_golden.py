@@ -84,3 +84,19 @@ def test_oracle_trace_snake_and_chains():
             lab[y, 0 if (y // 2) % 2 else w - 1] = 1
     lab[h - 1, 0] = 2
     assert O.trace(lab).sum() == (lab != 0).sum()
+
+
+LAPL = load("laplacian.npz")
+
+
+@pytest.mark.parametrize("name", [str(n) for n in LAPL["names"]])
+def test_oracle_laplacian_matches_reference(name):
+    """operator="laplacian" (bench.py:94-100): blur then the 5-point Laplacian
+    (gradient.py:93-107), both bit-exact against the reference's own outputs."""
+    arr = LAPL[f"{name}/input"]
+    for tag in ("s1.4", "s0.6"):
+        blurred = O.blur(arr, LAPL[f"{name}/{tag}/weights"])
+        assert np.array_equal(blurred, LAPL[f"{name}/{tag}/blurred"]), (name, tag)
+        assert np.array_equal(O.laplacian(blurred), LAPL[f"{name}/{tag}/response"]), (name, tag)
+    got = O.laplacian(O.blur(arr, LAPL[f"{name}/r2/weights"]))
+    assert np.array_equal(got, LAPL[f"{name}/r2/response"]), name
