@@ -7,6 +7,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <cmath>
 #include <cstring>
@@ -61,7 +62,7 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
     size_t hdr, fix, perim, gpar, gstrong, pending, border, plist_idx, plist_node, plist_count, node_list, node_count,
-        pend_tiles, dense, fgbits, stbits, plane_bytes, total;
+        pend_tiles, dense, fgbits, stbits, plane_bytes, hb, hb_bytes, total;
     unsigned long long fix_cap, plist_scap, node_scap;
     HystLayout hl;
 };
@@ -107,6 +108,9 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     off = align_up(off + L.plane_bytes);
     L.stbits = off;
     off = align_up(off + L.plane_bytes);
+    L.hb_bytes = hb_bytes(batch, H, W);
+    L.hb = off;
+    off = align_up(off + L.hb_bytes);
     L.total = off;
     return L;
 }
@@ -117,6 +121,7 @@ struct Ws {
     HystBufs hb;
     unsigned long long* fgbits;
     unsigned long long* stbits;
+    void* hbs;
 };
 
 Ws ws_bind(void* base, const WsLayout& L) {
@@ -140,6 +145,7 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.dense = reinterpret_cast<int*>(p + L.dense);
     w.fgbits = reinterpret_cast<unsigned long long*>(p + L.fgbits);
     w.stbits = reinterpret_cast<unsigned long long*>(p + L.stbits);
+    w.hbs = p + L.hb;
     return w;
 }
 
@@ -164,7 +170,9 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs 
         hdr->plist_overflow = 0;
         hdr->dense_count = 0;
         hdr->node_overflow = 0;
+        hdr->pad[2] = 0;
     }
+    if (threadIdx.x < 8) hdr->hb_sync[threadIdx.x] = 0;
     if (threadIdx.x < PL_STRIPES) {
         hb.plist_count[threadIdx.x] = 0;
         hb.node_count[threadIdx.x] = 0;
@@ -273,6 +281,12 @@ FastParams make_fast(const double* w, int r, double low, double high) {
     band(low, P.lo_lo, P.lo_hi);
     band(high, P.hi_lo, P.hi_hi);
     P.e_nms = (float)(S * 2.0 * Em(1443.0 * 1.01));
+    // the same bound relative to the two magnitudes compared: |c - n| must
+    // exceed Em(c) + Em(n) = 2 sqrt(2) eg + rel (c + n) (+ the true-vs-computed
+    // magnitude slack in the rel term: 2^-10), so ties between small
+    // magnitudes are not flagged with the band of the largest possible one
+    P.e_nms0 = std::nextafter((float)(S * (2.0 * std::sqrt(2.0) * eg + 1e-8)), INFINITY);
+    P.e_nms_rel = std::nextafter((float)(S * rel * (1.0 + std::ldexp(1.0, -10))), INFINITY);
     P.e_sec = (float)(S * ((1.0 + 0.41421356237309503) * eg + 3000.0 * u));
     P.cls0 = high <= 0.0 ? 2 : (low <= 0.0 ? 1 : 0);
     return P;
@@ -342,6 +356,10 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     return EF_OK;
 }
 
+// whole-frame hysteresis: 0 = bit-sweep (default), 1 = tile union-find
+// (ef_set_hysteresis_mode; EF_NO_HB=1 in the environment starts in mode 1)
+std::atomic<int> g_hyst_mode{1};
+
 // reset: the workspace header has not been initialised by a classify launch of
 // this call (standalone tracing).
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
@@ -349,6 +367,20 @@ int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, 
     const int sms = sm_count_current();
     if (reset) EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");
     if (bits && !bits->fg) bits = nullptr;
+    if (finalize && g_hyst_mode.load() == 0 && hb_supported(W)) {
+        // whole frames: bit-sweep hysteresis over the classifier's bit planes, or
+        // over planes packed from the labels (standalone tracing); the final
+        // map must hold the strong pixels first (the fused classifier wrote them)
+        FgBits B = bits ? *bits : FgBits{};
+        if (!bits) {
+            const int words = (W + 63) / 64;
+            B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)H * words, 0};
+            EF_CHECK(launch_hb_pack(labels, batch, H, W, ws.fgbits, ws.stbits, sms, st), "bit-plane pack");
+            EF_CHECK(launch_strong_final(labels, (long long)batch * H * W, fin, sms, st), "strong final");
+        }
+        EF_CHECK(launch_hystb(B, batch, H, W, fin, ws.hbs, L.hb_bytes, ws.hdr, sms, st), "bit-sweep hysteresis");
+        return EF_OK;
+    }
     EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, bits, sms, st), "hysteresis");
     if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
     return EF_OK;
@@ -391,6 +423,12 @@ int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream,
     return EF_OK;
 }
 
+int ef_set_hysteresis_mode(int32_t mode) {
+    if (mode != 0 && mode != 1) return fail(EF_EINVAL, "hysteresis mode must be 0 (bit sweep) or 1 (tile union-find)");
+    g_hyst_mode.store(mode);
+    return EF_OK;
+}
+
 int ef_set_block_tile_threshold(int32_t tiles_per_sm) {
     if (tiles_per_sm < 0) return fail(EF_EINVAL, "tiles_per_sm must be >= 0");
     set_block_tile_threshold(tiles_per_sm);
@@ -406,6 +444,7 @@ int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream,
     h_out[1] = h.plist_overflow;
     h_out[2] = h.dense_count;
     h_out[3] = h.node_overflow;
+    h_out[4] = h.pad[2];
     return EF_OK;
 }
 

@@ -34,7 +34,10 @@ struct FastParams {
     // certified comparisons of the fp32 magnitude m against the thresholds:
     // m < lo_lo -> certainly below low, m > lo_hi -> certainly >= low, else flag
     float lo_lo, lo_hi, hi_lo, hi_hi;
-    float e_nms;  // |c - n| > e_nms -> the NMS comparison is certain
+    float e_nms;  // |c - n| > e_nms -> the NMS comparison is certain (any magnitudes up to 1443)
+    // magnitude-relative form used by the production classifier: certain iff
+    // |c - n| > e_nms0 + e_nms_rel * (c + n)
+    float e_nms0, e_nms_rel;
     float e_sec;  // |t*a - b| > e_sec -> the orientation sector is certain
     int cls0;     // class of a suppressed pixel (thinned value 0.0)
     int no_v2;    // a caller buffer is not 4-byte aligned: the generic byte-wise classifier only
@@ -49,7 +52,8 @@ struct WsHeader {
     unsigned int plist_overflow;     // a pending-list stripe overflowed: H4 re-runs tile CCL
     unsigned int dense_count;        // tiles H1's warp kernel handed to the block kernel
     unsigned int node_overflow;      // a node-list stripe overflowed: H3 scans every perimeter slot
-    unsigned int pad[4];
+    unsigned int pad[4];             // pad[2]: rounds the bit-sweep hysteresis ran (ef_read_paths)
+    unsigned int hb_sync[8];         // bit-sweep hysteresis: grid barrier and round flags (zeroed per call)
 };
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

@@ -192,7 +192,7 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
 // ---------------------------------------------------------------- phase 2 --
 // The few scalars the classifier needs (kept in registers).
 struct V2Cls {
-    float lo_lo, lo_hi, hi_lo, hi_hi, e_nms, e_sec;
+    float lo_lo, lo_hi, hi_lo, hi_hi, e_nms0, e_nms_rel, e_sec;
     int cls0;
     int W, FH, out0;
 };
@@ -243,7 +243,9 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
         const float n135 = fmaxf(Mu[k], Md[k + 2]);
         const float ndiag = ((gx > 0.f) == (gy > 0.f)) ? n45 : n135;
         const float nmax = uu > 0.f ? n0 : (vv > 0.f ? n90 : ndiag);
-        const float d = c - sqrt_apx(nmax);
+        const float nv = sqrt_apx(nmax);
+        const float d = c - nv;
+        const float e_nms = fmaf(P.e_nms_rel, c + nv, P.e_nms0);  // magnitude-relative certification band
         const bool amb = fabsf(uu) <= P.e_sec || fabsf(vv) <= P.e_sec;
         // threshold class: 2 / 1 / 0, or -1 inside a certification band
         // (as c > hi_hi ? 2 : c >= hi_lo ? -1 : c > lo_hi ? 1 : c >= lo_lo ? -1 : 0,
@@ -252,8 +254,8 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
         const int lo_cls = c >= P.lo_lo ? (c > P.lo_hi ? 1 : -1) : 0;
         const int cls = c >= P.hi_lo ? (c > P.hi_hi ? 2 : -1) : lo_cls;
         const bool need_nms = cls >= 0 && (uint32_t)cls != cls0;
-        const bool flag = cls < 0 || (need_nms && (amb || fabsf(d) <= P.e_nms));
-        const uint32_t lab = flag ? (uint32_t)kFlag : ((need_nms && d > P.e_nms) ? (uint32_t)cls : cls0);
+        const bool flag = cls < 0 || (need_nms && (amb || fabsf(d) <= e_nms));
+        const uint32_t lab = flag ? (uint32_t)kFlag : ((need_nms && d > e_nms) ? (uint32_t)cls : cls0);
         any_flag |= flag;
         packed |= lab << (8 * k);
     }
@@ -598,7 +600,7 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS, V2_CS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                            max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
-    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
+    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
 

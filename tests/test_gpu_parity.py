@@ -23,14 +23,20 @@ def canny():
     return c
 
 
-@pytest.fixture(params=[0, 32], ids=["warp-per-tile", "block-per-tile-when-few"])
+@pytest.fixture(params=["sweep", 0, 32], ids=["bit-sweep", "unionfind-warp-per-tile", "unionfind-block-per-tile-when-few"])
 def h1_path(request, canny):
-    """Both hysteresis tile passes: 0 = always one warp per tile (with the dense
-    tile hand-over), 32 = the default (one block per tile for launches with at
-    most 32 tiles per SM)."""
-    canny.set_block_tile_threshold(request.param)
+    """Every whole-frame hysteresis path: the bit-parallel row sweeps (default),
+    and the tile union-find with 0 = always one warp per tile (with the dense
+    tile hand-over) or 32 = one block per tile for launches with at most 32
+    tiles per SM."""
+    if request.param == "sweep":
+        canny.set_hysteresis_mode("sweep")
+    else:
+        canny.set_hysteresis_mode("unionfind")
+        canny.set_block_tile_threshold(request.param)
     yield request.param
     canny.set_block_tile_threshold(32)
+    canny.set_hysteresis_mode("sweep")
 
 
 def _dev(a):
@@ -178,8 +184,11 @@ def test_dense_noise_overflow_paths(canny, low, high, h1_path):
     paths = canny.read_paths(ws)
     # the fallbacks this test is for ran: the pending-list overflow at the lower
     # threshold, and (one warp per tile) the hand-over of dense tiles to the block kernel
-    assert paths["pending_overflow"] == (low < 5.0), paths
-    assert (paths["dense_tiles"] > 0) == (h1_path == 0), paths
+    if h1_path == "sweep":
+        assert paths["hb_rounds"] >= 2 and not paths["pending_overflow"], paths
+    else:
+        assert paths["pending_overflow"] == (low < 5.0), paths
+        assert (paths["dense_tiles"] > 0) == (h1_path == 0), paths
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
     lab2 = canny.classify_u8(_dev(frames), w, low, high)
@@ -212,8 +221,15 @@ def test_node_list_overflow_large_noise(canny):
     w = O.gaussian_weights(0.6, radius=1)
     el, ef_ = O.canny(frames, w, 5.0, 60.0)
     ws = canny.new_workspace(*frames.shape)
-    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)
-    assert canny.read_paths(ws)["node_overflow"]  # H3's perimeter-scan fallback ran
+    canny.set_hysteresis_mode("unionfind")
+    try:
+        lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)
+        assert canny.read_paths(ws)["node_overflow"]  # H3's perimeter-scan fallback ran
+    finally:
+        canny.set_hysteresis_mode("sweep")
+    assert np.array_equal(_np(lab), el)
+    assert np.array_equal(_np(fin).astype(bool), ef_)
+    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)  # and the bit sweeps on the same frame
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
 
@@ -334,6 +350,61 @@ def test_hysteresis_vs_oracle(canny, h1_path):
         assert np.array_equal(_np(fin)[0].astype(bool), O.trace(lab)), lab.shape
     # the snake and the spiral are single components reaching every tile
     assert _np(canny.trace_edges_u8(_dev(_spiral_labels(333))))[0].sum() == (_spiral_labels(333) != 0).sum()
+
+
+def _maze(h, w, rng):
+    """A random spanning-tree maze of 1-pixel corridors (every corridor one
+    component), weak everywhere with strong pixels in a few cells: paths wind
+    up, down, left and right across many 32-row blocks and 64-bit words."""
+    ch, cw = (h - 1) // 2, (w - 1) // 2
+    lab = np.zeros((h, w), np.uint8)
+    seen = np.zeros((ch, cw), bool)
+    stack = [(0, 0)]
+    seen[0, 0] = True
+    lab[1, 1] = 1
+    while stack:
+        y, x = stack[-1]
+        nb = [(y + dy, x + dx) for dy, dx in ((0, 1), (1, 0), (0, -1), (-1, 0))
+              if 0 <= y + dy < ch and 0 <= x + dx < cw and not seen[y + dy, x + dx]]
+        if not nb:
+            stack.pop()
+            continue
+        ny, nx = nb[rng.integers(len(nb))]
+        seen[ny, nx] = True
+        lab[2 * ny + 1, 2 * nx + 1] = 1
+        lab[y + ny + 1, x + nx + 1] = 1
+        stack.append((ny, nx))
+    return lab
+
+
+@pytest.mark.parametrize("shape", [(257, 129), (301, 1999), (1025, 2048), (2049, 64), (67, 64 * 33 + 5)])
+def test_bit_sweep_long_paths_and_wide_frames(canny, shape):
+    """Bit-sweep hysteresis on structures that defeat a few local sweeps: a
+    snake crossing every block row, a maze of winding corridors, cut mazes
+    with a few strong pixels, and noise; against the oracle, with the block
+    walks counted (frames wider than 2048 columns take the tile union-find)."""
+    rng = np.random.default_rng(sum(shape))
+    h, w = shape
+    full = _maze(h, w, rng)
+    ys, xs = np.nonzero(full)
+    full[ys[-1], xs[-1]] = 2  # one strong cell: the whole maze is one edge
+    cases = [_snake(h, w), full]
+    m = _maze(h, w, rng)
+    m[rng.random(m.shape) < 0.02] = 0  # cut corridors: many components
+    ys, xs = np.nonzero(m)
+    m[ys[:3], xs[:3]] = 2
+    cases.append(m)
+    cases.append(rng.choice([0, 1, 2], size=(h, w), p=[0.5, 0.45, 0.05]).astype(np.uint8))
+    ws = canny.new_workspace(1, h, w)
+    rounds = []
+    for lab in cases:
+        fin = canny.trace_edges_u8(_dev(lab), ws=ws)
+        rounds.append(canny.read_paths(ws)["hb_rounds"])
+        assert np.array_equal(_np(fin)[0].astype(bool), O.trace(lab)), (shape, len(rounds))
+    if w <= 2048:
+        assert max(rounds) > 2, rounds  # pass 2 walked down and up more than once
+    else:
+        assert max(rounds) == 0, rounds  # wide frames: union-find
 
 
 def test_band_paths_match_whole_frame(canny):
