@@ -65,19 +65,11 @@ typedef struct ef_stats {
  * warp per tile.  The result is identical either way. */
 int ef_set_block_tile_threshold(int32_t tiles_per_sm);
 
-/* Whole-frame hysteresis algorithm (process-wide): 0 = bit-parallel row sweeps
- * over 1-bit-per-pixel planes with cross-block rounds (default), 1 = tile
- * union-find (H1-H4).  Row bands always use the union-find (their edge
- * components are merged across bands).  The result is identical either way. */
-int ef_set_hysteresis_mode(int32_t mode);
-
 /* Which capacity fallbacks the last call on this workspace took (synchronises
- * `stream`; h_out holds 5 entries): h_out[0] fix list overflowed (FX scanned
- * every label), [1] a pending-list stripe overflowed (H4 re-ran the pending
- * tiles), [2] tiles H1's warp kernel handed to the block kernel, [3] a
- * node-list stripe overflowed (H3 scanned every perimeter slot), [4] rounds of
- * cross-block propagation the bit-sweep hysteresis ran (fused whole-frame
- * path; 0 when the tile union-find ran).  For tests and diagnostics. */
+ * `stream`): h_out[0] fix list overflowed (FX scanned every label), [1] a
+ * pending-list stripe overflowed (H4 re-ran the pending tiles), [2] tiles H1's
+ * warp kernel handed to the block kernel, [3] a node-list stripe overflowed (H3
+ * scanned every perimeter slot).  For tests and diagnostics. */
 int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream, uint32_t* h_out);
 
 /* Bytes of device workspace needed by ef_canny_u8 / ef_canny_f64 /

@@ -287,19 +287,12 @@ def set_block_tile_threshold(tiles_per_sm: int) -> None:
     _lib.check(_lib.load().ef_set_block_tile_threshold(int(tiles_per_sm)), "ef_set_block_tile_threshold")
 
 
-def set_hysteresis_mode(mode: str) -> None:
-    """Whole-frame hysteresis: "sweep" (bit-parallel row sweeps, default) or
-    "unionfind" (tile union-find).  Identical results."""
-    code = {"sweep": 0, "unionfind": 1}[mode]
-    _lib.check(_lib.load().ef_set_hysteresis_mode(code), "ef_set_hysteresis_mode")
-
-
 def read_paths(ws, stream=None) -> dict:
     """Capacity fallbacks the last call on `ws` took (ef_read_paths)."""
-    out = (ctypes.c_uint32 * 5)()
+    out = (ctypes.c_uint32 * 4)()
     _lib.check(_lib.load().ef_read_paths(_ptr(ws), ws.numel(), _stream_ptr(stream), out), "ef_read_paths")
     return {"fix_overflow": bool(out[0]), "pending_overflow": bool(out[1]), "dense_tiles": int(out[2]),
-            "node_overflow": bool(out[3]), "hb_rounds": int(out[4])}
+            "node_overflow": bool(out[3])}
 
 
 def reset_stats(ws, stream=None) -> None:

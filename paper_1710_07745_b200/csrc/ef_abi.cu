@@ -62,7 +62,7 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct WsLayout {
     size_t hdr, fix, perim, gpar, gstrong, pending, border, plist_idx, plist_node, plist_count, node_list, node_count,
-        pend_tiles, dense, fgbits, stbits, plane_bytes, hb, hb_bytes, total;
+        pend_tiles, dense, fgbits, stbits, plane_bytes, total;
     unsigned long long fix_cap, plist_scap, node_scap;
     HystLayout hl;
 };
@@ -108,9 +108,6 @@ WsLayout ws_layout(int64_t batch, int H, int W) {
     off = align_up(off + L.plane_bytes);
     L.stbits = off;
     off = align_up(off + L.plane_bytes);
-    L.hb_bytes = hb_bytes(batch, H, W);
-    L.hb = off;
-    off = align_up(off + L.hb_bytes);
     L.total = off;
     return L;
 }
@@ -121,7 +118,6 @@ struct Ws {
     HystBufs hb;
     unsigned long long* fgbits;
     unsigned long long* stbits;
-    void* hbs;
 };
 
 Ws ws_bind(void* base, const WsLayout& L) {
@@ -145,7 +141,6 @@ Ws ws_bind(void* base, const WsLayout& L) {
     w.hb.dense = reinterpret_cast<int*>(p + L.dense);
     w.fgbits = reinterpret_cast<unsigned long long*>(p + L.fgbits);
     w.stbits = reinterpret_cast<unsigned long long*>(p + L.stbits);
-    w.hbs = p + L.hb;
     return w;
 }
 
@@ -170,9 +165,7 @@ __global__ void ws_begin_kernel(WsHeader* hdr, unsigned long long cap, HystBufs 
         hdr->plist_overflow = 0;
         hdr->dense_count = 0;
         hdr->node_overflow = 0;
-        hdr->pad[2] = 0;
     }
-    if (threadIdx.x < 8) hdr->hb_sync[threadIdx.x] = 0;
     if (threadIdx.x < PL_STRIPES) {
         hb.plist_count[threadIdx.x] = 0;
         hb.node_count[threadIdx.x] = 0;
@@ -356,10 +349,6 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     return EF_OK;
 }
 
-// whole-frame hysteresis: 0 = bit-sweep (default), 1 = tile union-find
-// (ef_set_hysteresis_mode; EF_NO_HB=1 in the environment starts in mode 1)
-std::atomic<int> g_hyst_mode{1};
-
 // reset: the workspace header has not been initialised by a classify launch of
 // this call (standalone tracing).
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
@@ -367,20 +356,6 @@ int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, 
     const int sms = sm_count_current();
     if (reset) EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");
     if (bits && !bits->fg) bits = nullptr;
-    if (finalize && g_hyst_mode.load() == 0 && hb_supported(W)) {
-        // whole frames: bit-sweep hysteresis over the classifier's bit planes, or
-        // over planes packed from the labels (standalone tracing); the final
-        // map must hold the strong pixels first (the fused classifier wrote them)
-        FgBits B = bits ? *bits : FgBits{};
-        if (!bits) {
-            const int words = (W + 63) / 64;
-            B = FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)H * words, 0};
-            EF_CHECK(launch_hb_pack(labels, batch, H, W, ws.fgbits, ws.stbits, sms, st), "bit-plane pack");
-            EF_CHECK(launch_strong_final(labels, (long long)batch * H * W, fin, sms, st), "strong final");
-        }
-        EF_CHECK(launch_hystb(B, batch, H, W, fin, ws.hbs, L.hb_bytes, ws.hdr, sms, st), "bit-sweep hysteresis");
-        return EF_OK;
-    }
     EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, bits, sms, st), "hysteresis");
     if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
     return EF_OK;
@@ -423,12 +398,6 @@ int ef_read_stats(const void* d_workspace, size_t workspace_bytes, void* stream,
     return EF_OK;
 }
 
-int ef_set_hysteresis_mode(int32_t mode) {
-    if (mode != 0 && mode != 1) return fail(EF_EINVAL, "hysteresis mode must be 0 (bit sweep) or 1 (tile union-find)");
-    g_hyst_mode.store(mode);
-    return EF_OK;
-}
-
 int ef_set_block_tile_threshold(int32_t tiles_per_sm) {
     if (tiles_per_sm < 0) return fail(EF_EINVAL, "tiles_per_sm must be >= 0");
     set_block_tile_threshold(tiles_per_sm);
@@ -444,7 +413,6 @@ int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream,
     h_out[1] = h.plist_overflow;
     h_out[2] = h.dense_count;
     h_out[3] = h.node_overflow;
-    h_out[4] = h.pad[2];
     return EF_OK;
 }
 

@@ -52,8 +52,7 @@ struct WsHeader {
     unsigned int plist_overflow;     // a pending-list stripe overflowed: H4 re-runs tile CCL
     unsigned int dense_count;        // tiles H1's warp kernel handed to the block kernel
     unsigned int node_overflow;      // a node-list stripe overflowed: H3 scans every perimeter slot
-    unsigned int pad[4];             // pad[2]: rounds the bit-sweep hysteresis ran (ef_read_paths)
-    unsigned int hb_sync[8];         // bit-sweep hysteresis: grid barrier and round flags (zeroed per call)
+    unsigned int pad[4];
 };
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

@@ -138,15 +138,6 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                               cudaStream_t st);
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st);
-// Bit-sweep hysteresis over the classifier's bit planes (whole frames, fused
-// path): workspace bytes and the launch (one cooperative kernel).
-bool hb_supported(int W);  // frames up to 2048 columns
-size_t hb_bytes(int64_t batch, int H, int W);
-cudaError_t launch_hystb(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, void* buf, size_t bytes,
-                         WsHeader* hdr, int sm_count, cudaStream_t st);
-cudaError_t launch_hb_pack(const uint8_t* labels, int64_t batch, int H, int W, unsigned long long* fg,
-                           unsigned long long* st, int sm_count, cudaStream_t st_);
-cudaError_t launch_strong_final(const uint8_t* labels, long long n, uint8_t* fin, int sm_count, cudaStream_t st);
 cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
                               cudaStream_t st);
 cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,

@@ -23,20 +23,14 @@ def canny():
     return c
 
 
-@pytest.fixture(params=["sweep", 0, 32], ids=["bit-sweep", "unionfind-warp-per-tile", "unionfind-block-per-tile-when-few"])
+@pytest.fixture(params=[0, 32], ids=["warp-per-tile", "block-per-tile-when-few"])
 def h1_path(request, canny):
-    """Every whole-frame hysteresis path: the bit-parallel row sweeps (default),
-    and the tile union-find with 0 = always one warp per tile (with the dense
-    tile hand-over) or 32 = one block per tile for launches with at most 32
-    tiles per SM."""
-    if request.param == "sweep":
-        canny.set_hysteresis_mode("sweep")
-    else:
-        canny.set_hysteresis_mode("unionfind")
-        canny.set_block_tile_threshold(request.param)
+    """Both hysteresis tile passes: 0 = always one warp per tile (with the dense
+    tile hand-over), 32 = the default (one block per tile for launches with at
+    most 32 tiles per SM)."""
+    canny.set_block_tile_threshold(request.param)
     yield request.param
     canny.set_block_tile_threshold(32)
-    canny.set_hysteresis_mode("sweep")
 
 
 def _dev(a):
@@ -184,11 +178,8 @@ def test_dense_noise_overflow_paths(canny, low, high, h1_path):
     paths = canny.read_paths(ws)
     # the fallbacks this test is for ran: the pending-list overflow at the lower
     # threshold, and (one warp per tile) the hand-over of dense tiles to the block kernel
-    if h1_path == "sweep":
-        assert paths["hb_rounds"] >= 2 and not paths["pending_overflow"], paths
-    else:
-        assert paths["pending_overflow"] == (low < 5.0), paths
-        assert (paths["dense_tiles"] > 0) == (h1_path == 0), paths
+    assert paths["pending_overflow"] == (low < 5.0), paths
+    assert (paths["dense_tiles"] > 0) == (h1_path == 0), paths
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
     lab2 = canny.classify_u8(_dev(frames), w, low, high)
@@ -221,15 +212,8 @@ def test_node_list_overflow_large_noise(canny):
     w = O.gaussian_weights(0.6, radius=1)
     el, ef_ = O.canny(frames, w, 5.0, 60.0)
     ws = canny.new_workspace(*frames.shape)
-    canny.set_hysteresis_mode("unionfind")
-    try:
-        lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)
-        assert canny.read_paths(ws)["node_overflow"]  # H3's perimeter-scan fallback ran
-    finally:
-        canny.set_hysteresis_mode("sweep")
-    assert np.array_equal(_np(lab), el)
-    assert np.array_equal(_np(fin).astype(bool), ef_)
-    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)  # and the bit sweeps on the same frame
+    lab, fin = canny.canny_u8(_dev(frames), w, 5.0, 60.0, ws=ws)
+    assert canny.read_paths(ws)["node_overflow"]  # H3's perimeter-scan fallback ran
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
 
@@ -353,9 +337,8 @@ def test_hysteresis_vs_oracle(canny, h1_path):
 
 
 def _maze(h, w, rng):
-    """A random spanning-tree maze of 1-pixel corridors (every corridor one
-    component), weak everywhere with strong pixels in a few cells: paths wind
-    up, down, left and right across many 32-row blocks and 64-bit words."""
+    """A random spanning-tree maze of 1-pixel corridors (one component), weak
+    everywhere: paths wind up, down, left and right across many tiles."""
     ch, cw = (h - 1) // 2, (w - 1) // 2
     lab = np.zeros((h, w), np.uint8)
     seen = np.zeros((ch, cw), bool)
@@ -377,34 +360,24 @@ def _maze(h, w, rng):
     return lab
 
 
-@pytest.mark.parametrize("shape", [(257, 129), (301, 1999), (1025, 2048), (2049, 64), (67, 64 * 33 + 5)])
-def test_bit_sweep_long_paths_and_wide_frames(canny, shape):
-    """Bit-sweep hysteresis on structures that defeat a few local sweeps: a
-    snake crossing every block row, a maze of winding corridors, cut mazes
-    with a few strong pixels, and noise; against the oracle, with the block
-    walks counted (frames wider than 2048 columns take the tile union-find)."""
+@pytest.mark.parametrize("shape", [(257, 129), (301, 1999), (1025, 2048), (67, 64 * 33 + 5)])
+def test_hysteresis_mazes_vs_oracle(canny, shape, h1_path):
+    """Long winding weak paths: a maze whose one strong cell makes the whole
+    maze an edge, mazes cut into many components with a few strong cells, and
+    a snake -- against the oracle."""
     rng = np.random.default_rng(sum(shape))
     h, w = shape
     full = _maze(h, w, rng)
     ys, xs = np.nonzero(full)
-    full[ys[-1], xs[-1]] = 2  # one strong cell: the whole maze is one edge
-    cases = [_snake(h, w), full]
-    m = _maze(h, w, rng)
-    m[rng.random(m.shape) < 0.02] = 0  # cut corridors: many components
-    ys, xs = np.nonzero(m)
-    m[ys[:3], xs[:3]] = 2
-    cases.append(m)
-    cases.append(rng.choice([0, 1, 2], size=(h, w), p=[0.5, 0.45, 0.05]).astype(np.uint8))
-    ws = canny.new_workspace(1, h, w)
-    rounds = []
-    for lab in cases:
-        fin = canny.trace_edges_u8(_dev(lab), ws=ws)
-        rounds.append(canny.read_paths(ws)["hb_rounds"])
-        assert np.array_equal(_np(fin)[0].astype(bool), O.trace(lab)), (shape, len(rounds))
-    if w <= 2048:
-        assert max(rounds) > 2, rounds  # pass 2 walked down and up more than once
-    else:
-        assert max(rounds) == 0, rounds  # wide frames: union-find
+    full[ys[-1], xs[-1]] = 2
+    cut = _maze(h, w, rng)
+    cut[rng.random(cut.shape) < 0.02] = 0
+    ys, xs = np.nonzero(cut)
+    cut[ys[:3], xs[:3]] = 2
+    for lab in (full, cut, _snake(h, w)):
+        fin = canny.trace_edges_u8(_dev(lab))
+        assert np.array_equal(_np(fin)[0].astype(bool), O.trace(lab)), shape
+    assert _np(canny.trace_edges_u8(_dev(full)))[0].sum() == (full != 0).sum()
 
 
 def test_band_paths_match_whole_frame(canny):
