@@ -235,6 +235,67 @@ def cpu_baseline(frames, weights, low, high):
                       f"{cores} threads"}
 
 
+def reference_python_baseline(frames, radius, low, high, budget_s=12.0):
+    """The reference itself (pure Python edgeforge, installed unmodified into
+    baseline/_ref) on a stated subset of the workload: its own stage functions
+    in run_pipeline's order (bench.py:61-126) with the configs' radius-2
+    GaussianKernel, WorkerConfig(workers=all host cores), serial hysteresis;
+    1 warm-up + median of 3 (run_benchmark's method, bench.py:233-290)."""
+    import platform
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "edgeforge")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import numpy as np
+        import scipy
+
+        import edgeforge as E
+        from edgeforge.filtering import GaussianKernel
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        sys.path.remove(ref)
+    cores = len(os.sched_getaffinity(0))
+    x = np.arange(-radius, radius + 1, dtype=np.float64)
+    w = np.exp(-(x * x) / (2.0 * 1.4 * 1.4))
+    w /= w.sum()
+    kern = GaussianKernel(sigma=1.4, radius=radius, weights=w)
+    wc = E.WorkerConfig(workers=cores)
+    t = E.Thresholds(low=low, high=high)
+
+    def one(f):
+        img = E.GrayImage.from_array(f.astype(np.float64))
+        blurred = E.gaussian_blur(img, kern, wc)
+        thin = E.non_max_suppress(E.sobel(blurred, wc), wc)
+        return E.trace_edges(E.double_threshold(thin, t))
+
+    one(frames[0])  # warm-up
+    t0 = time.perf_counter()
+    one(frames[0])
+    per_frame = time.perf_counter() - t0
+    n = max(1, min(len(frames), int(budget_s / 3 / max(per_frame, 1e-3))))
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for f in frames[:n]:
+            one(f)
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    try:
+        cpu = next(line.split(":", 1)[1].strip() for line in open("/proc/cpuinfo") if line.startswith("model name"))
+    except (OSError, StopIteration):
+        cpu = platform.processor()
+    return {"value": round(n * frames[0].size / 1e6 / dt, 3), "unit": "MP/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{n} of the workload's frames per rep, 1 warm-up + median of 3; the reference's stage functions "
+                      f"(gaussian_blur, sobel, non_max_suppress, double_threshold, trace_edges) with "
+                      f"GaussianKernel(1.4, radius {radius}), WorkerConfig(workers={cores}), serial hysteresis",
+            "host": {"cpu": cpu, "python": platform.python_version(), "numpy": np.__version__,
+                     "scipy": scipy.__version__}}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -554,6 +615,8 @@ def run_ours(args):
     if rank == 0:
         # the CPU baseline is timed on rank 0 at N=1 only (a reported baseline, not per-rank work)
         cpu = None if (args.no_cpu or world > 1) else cpu_baseline(frames, w, low, high)
+        if cpu is not None:
+            cpu["reference_python"] = reference_python_baseline(frames, args.radius, low, high)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,

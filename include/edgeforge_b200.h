@@ -197,6 +197,14 @@ int ef_ipc_export(const void* d_ptr, void* h_handle64, uint64_t* h_offset);
 int ef_ipc_open(const void* h_handle64, uint64_t offset, void** d_ptr_out, void** d_base_out);
 int ef_ipc_close(void* d_base);
 
+/* Stream-ordered 32-bit flags for the peer-halo handshake (device side, no
+ * host synchronisation): ef_stream_write_u32 stores `value` at d_addr once the
+ * stream's earlier work is complete and visible; ef_stream_wait_u32 makes the
+ * stream's later work wait until *d_addr >= value.  d_addr may be an IPC / peer
+ * mapping of another rank's flags.  4-byte aligned. */
+int ef_stream_write_u32(void* d_addr, uint32_t value, void* stream);
+int ef_stream_wait_u32(const void* d_addr, uint32_t value, void* stream);
+
 /* Band-local hysteresis only, for labels already computed (the per-band
  * labelling of trace_edges_parallel, hysteresis.py:97-101). */
 int ef_band_trace(const uint8_t* d_labels, int32_t rows, int32_t width, uint8_t* d_final, void* d_workspace,
@@ -230,6 +238,28 @@ int ef_band_merge_device(int32_t nbands, int32_t width, const int64_t* d_ids, co
 int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width,
                      const uint8_t* d_labels, uint8_t* d_final, void* d_workspace,
                      size_t workspace_bytes, void* stream);
+
+/* ---- PGM ingest / egress (image.py:87-135; the CLI detect path cli.py:82-90).
+ * Host parsing and decoding straight to u8 (no float64 image); errors return
+ * EF_EINVAL with the reference's PgmFormatError message in
+ * ef_pgm_last_error() and its byte offset in *err_offset. */
+typedef struct ef_pgm_info {
+    int32_t width, height, maxval;
+    int32_t binary;          /* 1: P5 (payload_offset = first payload byte), 0: P2 */
+    int64_t payload_offset;  /* P2: where the pixel tokens start */
+} ef_pgm_info;
+
+const char* ef_pgm_last_error(void);
+/* Parse the header (magic, width, height, maxval; P5: the payload length). */
+int ef_pgm_parse(const uint8_t* data, size_t n, ef_pgm_info* info, int64_t* err_offset);
+/* Decode the width*height pixels into h_dst (host memory, e.g. pinned) and
+ * check them against maxval. */
+int ef_pgm_decode_u8(const uint8_t* data, size_t n, const ef_pgm_info* info, uint8_t* h_dst, int64_t* err_offset);
+/* "P5\n<w> <h>\n255\n" into h_out; returns its length (or EF_EINVAL). */
+int ef_pgm_header(int32_t width, int32_t height, char* h_out, size_t cap);
+/* P5 payload of an edge map on the device: 255 where d_final != 0, else 0
+ * (save_pgm(edges_to_image(edges)), bench.py:129-133 + image.py:125-135). */
+int ef_pgm_encode_edges(const uint8_t* d_final, int64_t n, uint8_t* d_payload, void* stream);
 
 #ifdef __cplusplus
 }

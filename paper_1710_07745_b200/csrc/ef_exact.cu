@@ -1,3 +1,4 @@
+#include <algorithm>
 // ef_exact.cu -- exact float64 kernels in the reference's operation order.
 //
 //  ex_tile_kernel   full-frame exact pipeline on a tile (u8 or float64 input):
@@ -356,8 +357,12 @@ cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, co
                        int sm_count, cudaStream_t st) {
     auto kern = (g.top || g.bot) ? fix_kernel<true> : fix_kernel<false>;
     const size_t smem = (size_t)FX_GROUPS * fx_group_bytes(P.r);
-    return launch_pdl(kern, dim3(sm_count * 16), dim3(FX_WARPS * 32), smem, st, src, batch, g, P, labels, list, hdr,
-                      B);
+    // small launches get a small grid (the kernel grid-strides over the list, or
+    // over every pixel when the list overflowed): 2368 mostly idle blocks cost
+    // a 512x512 frame ~5 us
+    const long long px = batch * (long long)g.rows * g.W;
+    const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((long long)sm_count * 16, px / 4096));
+    return launch_pdl(kern, dim3(blocks), dim3(FX_WARPS * 32), smem, st, src, batch, g, P, labels, list, hdr, B);
 }
 
 }  // namespace ef

@@ -1058,6 +1058,12 @@ __global__ void band_apply_kernel(int rows, int W, int tiles_x, int tiles_y, con
 }
 
 // ---------------------------------------------------------------------------
+// blocks per list stripe for H3 / H4: sm_count / 4 for large launches, fewer
+// for small ones (one 512x512 frame has 64 tiles; 2368 blocks were ~3 us each)
+static unsigned stripe_blocks(int64_t tiles, int sm_count) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(std::max(1, sm_count / 4), tiles / 256));
+}
+
 HystLayout hyst_layout(int64_t batch, int H, int W) {
     HystLayout L;
     L.tiles_x = (W + HT - 1) / HT;
@@ -1118,20 +1124,22 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
         e = launch_pdl(hyst_local_warp_kernel<false>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
                        L.tiles_y, final_out, b, hdr, FgBits{});
     if (e != cudaSuccess) return e;
-    e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x, L.tiles_y,
-                   final_out, b, hdr);
-    if (e != cudaSuccess) return e;
+    if (!allblock) {  // the block kernel took every tile: the dense list is empty
+        e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x,
+                       L.tiles_y, final_out, b, hdr);
+        if (e != cudaSuccess) return e;
+    }
     const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);
     e = launch_pdl(hyst_merge_kernel, mgrid, dim3(256), 0, st, H, W, L.tiles_x, L.tiles_y, b);
     if (e != cudaSuccess) return e;
-    return launch_pdl(hyst_resolve_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), dim3(256), 0, st,
+    return launch_pdl(hyst_resolve_kernel, dim3(stripe_blocks(L.tiles, sm_count), PL_STRIPES), dim3(256), 0, st,
                       (long long)L.slots, b, hdr);
 }
 
 cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
                               const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    return launch_pdl(hyst_final_kernel, dim3((unsigned)std::max(1, sm_count / 4), PL_STRIPES), dim3(H_THREADS), 0,
+    return launch_pdl(hyst_final_kernel, dim3(stripe_blocks(L.tiles, sm_count), PL_STRIPES), dim3(H_THREADS), 0,
                       st, labels, H, W, L.tiles_x, L.tiles_y, (int)batch, final_out, b, hdr);
 }
 

@@ -147,6 +147,51 @@ def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming]
     return result
 
 
+def detect_pgm(data: bytes, cfg: PipelineConfig) -> bytes:
+    """The CLI's detect path (cli.py:82-90) as one call: PGM bytes in, P5
+    bytes of the edge map out -- equal to
+    save_pgm(edges_to_image(run_pipeline(load_pgm(data), cfg).edges)), or for
+    operator="laplacian" to save_pgm(rescale_for_view(response)).
+
+    Canny: the pixels are decoded straight into pinned host memory as bytes
+    (no float64 image), cross PCIe at 1 B/px, the edge map is encoded as the
+    0/255 payload on the device, and only that payload comes back."""
+    import ctypes
+
+    from . import _lib, canny
+    from .image import decode_pgm_u8, pgm_header
+
+    torch = canny.require_cuda()
+    if cfg.operator != "canny":
+        from .image import load_pgm, save_pgm
+
+        res = run_pipeline(load_pgm(data), cfg)
+        return save_pgm(rescale_for_view(res.response.pixels))
+    # header first (errors before any device work), then the pixels into pinned memory
+    info = _lib.EfPgmInfo()
+    off = ctypes.c_int64(0)
+    buf = bytes(data)
+    rc = _lib.load().ef_pgm_parse(buf, len(buf), ctypes.byref(info), ctypes.byref(off))
+    if rc != _lib.EF_OK:
+        decode_pgm_u8(buf)  # raises the PgmFormatError
+    h, w = info.height, info.width
+    pinned = torch.empty((h, w), dtype=torch.uint8).pin_memory()
+    decode_pgm_u8(buf, out=pinned.numpy())
+    src = pinned.to("cuda", non_blocking=True)
+    weights = cfg.kernel().weights
+    thresholds = cfg.thresholds
+    if thresholds is None:
+        thresholds = _auto_from_peak(canny.thinned_max(src, weights))
+    _, final = canny.canny_u8(src, weights, thresholds.low, thresholds.high)
+    payload = torch.empty(h * w, dtype=torch.uint8, device=src.device)
+    st = int(torch.cuda.current_stream().cuda_stream)
+    _lib.check(_lib.load().ef_pgm_encode_edges(final.data_ptr(), h * w, payload.data_ptr(), st), "ef_pgm_encode_edges")
+    out = torch.empty(h * w, dtype=torch.uint8).pin_memory()
+    out.copy_(payload, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return pgm_header(w, h) + out.numpy().tobytes()
+
+
 def edges_to_image(edges: EdgeMap) -> GrayImage:
     """Binary edge map as a 0/255 image (bench.py:129-133)."""
     if edges.final is None:

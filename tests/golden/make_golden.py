@@ -18,11 +18,15 @@ Fixtures:
                 the reference default radius 5; inputs are pinned by sha256.
   quantize.npz  quantize_orientation on axis, diagonal and near-boundary
                 gradient pairs.
+  pgm.npz       load_pgm on a seeded corpus of valid and malformed P5/P2 files
+                (pixels, or PgmFormatError message + offset), save_pgm bytes,
+                and the CLI detect path's output bytes
+                save_pgm(edges_to_image(run_pipeline(load_pgm(f), cfg).edges)).
   laplacian.npz run_pipeline(operator="laplacian", keep_intermediates=True)
                 response + blurred for the fixture set (sigma 1.4 and 0.6), and
                 gaussian_blur -> laplacian with the configs' radius-2 kernel.
 
-    python tests/golden/make_golden.py [stages pipeline configs quantize laplacian]
+    python tests/golden/make_golden.py [stages pipeline configs quantize laplacian pgm]
 """
 
 from __future__ import annotations
@@ -133,11 +137,89 @@ def make_laplacian():
     print("laplacian.npz", os.path.getsize(os.path.join(HERE, "laplacian.npz")))
 
 
+def pgm_corpus():
+    """Seeded PGM byte strings: valid files with comments, odd whitespace,
+    small maxval, trailing bytes; and malformed ones (own corpus)."""
+    rng = np.random.default_rng(1710)
+    out = []
+
+    def p5(w, h, px, maxval=255, sep=b"\n", pre=b""):
+        return pre + b"P5" + sep + f"{w} {h}".encode() + sep + str(maxval).encode() + b"\n" + bytes(px)
+
+    def p2(w, h, px, maxval=255, sep=b" "):
+        return b"P2\n" + f"{w} {h}".encode() + b"\n" + str(maxval).encode() + b"\n" + sep.join(
+            str(int(v)).encode() for v in px)
+
+    for (w, h) in [(1, 1), (3, 2), (17, 5), (64, 48), (33, 33)]:
+        px = rng.integers(0, 256, w * h)
+        out.append(p5(w, h, px))
+        out.append(p5(w, h, px, sep=b" # a comment\n\t"))
+        out.append(p5(w, h, px, pre=b"# leading comment\n") + b"trailing bytes")
+        out.append(p2(w, h, px))
+        out.append(p2(w, h, px, sep=b"\n#c\n"))
+        small = rng.integers(0, 8, w * h)
+        out.append(p5(w, h, small, maxval=7))
+        out.append(p2(w, h, small, maxval=7))
+    base = p5(6, 4, rng.integers(0, 256, 24))
+    bad = [b"", b"   ", b"# only a comment", b"P6\n1 1\n255\n\x00", b"P5", b"P5 3", b"P5 3 2", b"P5 3 2 255",
+           b"P5 3 2 255\x01\x02", b"P5\n3 2\n255\n\x00\x01", b"P5 0 2 255 ", b"P5 2 0 255 ", b"P5 2 2 0 ",
+           b"P5 2 2 256 ", b"P5 2 2 1000 ", b"P5 -2 2 255 ", b"P5 2x 2 255 ", b"P5 2 2 2.5 ", b"P5 2 2 255#c\n1234",
+           b"p5 2 2 255 1234", b"P2 2 2 255 1 2 3", b"P2 2 2 255 1 2 3 x", b"P2 2 2 9 1 2 3 10", b"P2 1 1 255 +5",
+           b"P2 2 1 3 3 4", b"P5 2 2 7 \x00\x01\x08\x02", b"\xffP5 1 1 255 \x00", b"P5 b'q' 1 255 ",
+           b'P5 a"b 1 255 ', b"P5 a'b 1 255 ", b"P5 \\x 1 255 ", b"P5 1 1 255\t\x07", b"P5 2 2 255 \x01",
+           b"P25 2 2 255 ", b"P2 3 1 255 1 2#3\n4", base[:-1], base + b"\x00"]
+    for i in range(40):  # truncations and single-byte corruptions of a valid file
+        b = bytearray(base)
+        if i % 2:
+            b = b[: int(rng.integers(0, len(b)))]
+        else:
+            b[int(rng.integers(0, 16))] = int(rng.integers(0, 256))
+        bad.append(bytes(b))
+    return out + bad
+
+
+def make_pgm():
+    from edgeforge.bench import edges_to_image, run_pipeline
+
+    out = {}
+    corpus = pgm_corpus()
+    for i, data in enumerate(corpus):
+        out[f"in/{i}"] = np.frombuffer(data, np.uint8)
+        try:
+            img = ef.load_pgm(data)
+        except ef.PgmFormatError as err:
+            out[f"err/{i}"] = np.array(str(err))
+            out[f"off/{i}"] = np.array(err.offset)
+            continue
+        out[f"px/{i}"] = img.pixels.astype(np.uint8)
+        out[f"save/{i}"] = np.frombuffer(ef.save_pgm(img), np.uint8)
+    out["n"] = np.array(len(corpus))
+    # the CLI detect path on P5 inputs: edges -> 0/255 P5 bytes
+    rng = np.random.default_rng(77)
+    det = []
+    for k, arr in enumerate([synth.config0()[:160, :200], synth.config3_image(7)[:128, :256],
+                             rng.integers(0, 256, (45, 67)).astype(np.uint8)]):
+        data = b"P5\n%d %d\n255\n" % (arr.shape[1], arr.shape[0]) + arr.tobytes()
+        for tag, cfg in (("t2050", ef.PipelineConfig(sigma=1.4, thresholds=ef.Thresholds(20.0, 50.0))),
+                         ("auto", ef.PipelineConfig(sigma=1.4)),
+                         ("s2_par", ef.PipelineConfig(sigma=2.0, thresholds=ef.Thresholds(10.0, 30.0),
+                                                      hysteresis_mode="parallel"))):
+            res = run_pipeline(ef.load_pgm(data), cfg)
+            out[f"det/{k}/{tag}/in"] = np.frombuffer(data, np.uint8)
+            out[f"det/{k}/{tag}/out"] = np.frombuffer(ef.save_pgm(edges_to_image(res.edges)), np.uint8)
+            det.append(f"{k}/{tag}")
+    out["det"] = np.array(det)
+    np.savez_compressed(os.path.join(HERE, "pgm.npz"), **out)
+    print("pgm.npz", os.path.getsize(os.path.join(HERE, "pgm.npz")), len(corpus), "files")
+
+
 def main():
-    which = set(sys.argv[1:]) or {"stages", "pipeline", "configs", "quantize", "laplacian"}
+    which = set(sys.argv[1:]) or {"stages", "pipeline", "configs", "quantize", "laplacian", "pgm"}
     if "laplacian" in which:
         make_laplacian()
-    if which <= {"laplacian"}:
+    if "pgm" in which:
+        make_pgm()
+    if which <= {"laplacian", "pgm"}:
         return
     out = {}
     # ---------------- stages ----------------

@@ -257,3 +257,28 @@ def test_band_meta_must_be_contiguous_in_rank_order():
                     ([(0, 0), (0, 16)], 16)):
         with pytest.raises(ValueError):
             bands.check_band_meta(meta, h)
+
+
+def test_pgm_codec_matches_reference_corpus():
+    """load_pgm / save_pgm (image.py:87-135) against the reference's own results
+    on a seeded corpus of valid and malformed files: pixels, PgmFormatError
+    message and byte offset, save_pgm bytes.  Host parsing in the library."""
+    from golden_data import load
+
+    g = load("pgm.npz")
+    n_ok = n_err = 0
+    for i in range(int(g["n"])):
+        data = g[f"in/{i}"].tobytes()
+        if f"err/{i}" in g.files:
+            with pytest.raises(ef.PgmFormatError) as ei:
+                ef.load_pgm(data)
+            assert str(ei.value) == str(g[f"err/{i}"]), (i, data[:40])
+            assert ei.value.offset == int(g[f"off/{i}"]), (i, data[:40])
+            n_err += 1
+        else:
+            img = ef.load_pgm(data)
+            assert img.pixels.dtype == np.float64 and np.array_equal(img.pixels, g[f"px/{i}"]), i
+            assert ef.save_pgm(img) == g[f"save/{i}"].tobytes(), i
+            assert np.array_equal(ef.decode_pgm_u8(data), g[f"px/{i}"]), i
+            n_ok += 1
+    assert n_ok >= 30 and n_err >= 40

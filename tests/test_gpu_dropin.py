@@ -147,3 +147,24 @@ def test_full_config3_all_1024_frames_vs_oracle():
     bad = np.nonzero((lab != el).reshape(len(frames), -1).any(1) | (fin != ef_).reshape(len(frames), -1).any(1))[0]
     assert bad.size == 0, f"frames differing from the oracle: {bad[:20].tolist()}"
     print(f"C3 1024 frames: strong={int((el == 2).sum())} final={int(ef_.sum())} stats={stats}")
+
+
+def test_detect_pgm_matches_reference_cli_bytes(ef):
+    """The CLI detect path (cli.py:82-90): PGM bytes -> edge-map P5 bytes,
+    decoded into pinned memory as u8, encoded 0/255 on the device -- byte for
+    byte the reference's save_pgm(edges_to_image(run_pipeline(...).edges)),
+    with explicit and auto thresholds and parallel hysteresis."""
+    g = load("pgm.npz")
+    cfgs = {"t2050": ef.PipelineConfig(sigma=1.4, thresholds=ef.Thresholds(20.0, 50.0)),
+            "auto": ef.PipelineConfig(sigma=1.4),
+            "s2_par": ef.PipelineConfig(sigma=2.0, thresholds=ef.Thresholds(10.0, 30.0), hysteresis_mode="parallel")}
+    for key in [str(k) for k in g["det"]]:
+        tag = key.split("/")[1]
+        data = g[f"det/{key}/in"].tobytes()
+        want = g[f"det/{key}/out"].tobytes()
+        assert ef.detect_pgm(data, cfgs[tag]) == want, key
+        # the same through the drop-in stage API
+        res = ef.run_pipeline(ef.load_pgm(data), cfgs[tag])
+        assert ef.save_pgm(ef.edges_to_image(res.edges)) == want, key
+    with pytest.raises(ef.PgmFormatError):
+        ef.detect_pgm(b"P5 2 2 255 \x00", cfgs["t2050"])

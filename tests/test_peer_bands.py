@@ -6,8 +6,12 @@ The ranks are separate processes that share one GPU here (gpurun gives one
 B200): each maps its neighbours' band buffers over CUDA IPC exactly as it would
 map another GPU's (where the loads then travel over NVLink), and the group is
 gloo (NCCL refuses two ranks on one device).  No rank's kernel waits on another
-rank's kernel: bands are written, the group synchronises, then every rank reads.
-The assembled result must equal the whole-frame call bit for bit.
+rank's kernel: ordering is a stream-ordered handshake through IPC-mapped flags
+(a rank's stream waits for its neighbours' "band written" flags before its
+classifier reads their rows, and for their "rows read" flags before it
+overwrites its own band).  The assembled result must equal the whole-frame
+call bit for bit, also when every rank writes a new frame into its band
+between calls with no host synchronisation in between.
 """
 
 import os
@@ -29,7 +33,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, frame, plan, weights, low, high, steps, out):
+def _worker(rank, world, port, frames, plan, weights, low, high, steps, out):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -40,13 +44,17 @@ def _worker(rank, world, port, frame, plan, weights, low, high, steps, out):
         from paper_1710_07745_b200 import bands
 
         s, e = plan[rank]
-        band = torch.from_numpy(np.ascontiguousarray(frame[s:e])).cuda()
-        be = bands.CudaBandBackend(e - s, frame.shape[1])
-        for _ in range(steps):  # repeated calls reuse the mappings
-            lab, fin = bands.distributed_band_canny(band, s, frame.shape[0], weights, low, high, backend=be,
-                                                    peer=True)
+        h, w = frames[0].shape
+        src = torch.from_numpy(np.ascontiguousarray(np.stack([f[s:e] for f in frames]))).cuda()
+        band = torch.empty((e - s, w), dtype=torch.uint8, device="cuda")
+        be = bands.CudaBandBackend(e - s, w)
+        res = []
+        for step in range(steps):  # a new frame every call, written on this rank's stream
+            band.copy_(src[step % len(frames)])
+            lab, fin = bands.distributed_band_canny(band, s, h, weights, low, high, backend=be, peer=True)
+            res.append((lab.clone(), fin.clone()))  # stream-ordered snapshot, no host sync
         torch.cuda.synchronize()
-        out[rank] = (lab.cpu().numpy().copy(), fin.cpu().numpy().copy())
+        out[rank] = [(a.cpu().numpy().copy(), b.cpu().numpy().copy()) for a, b in res]
         dist.barrier()  # nobody unmaps a band another rank may still be reading
         be.close_peers()
     finally:
@@ -60,18 +68,47 @@ def test_peer_halo_bands_match_whole_frame(world, radius):
     from paper_1710_07745_b200 import bands, canny, synth
     from paper_1710_07745_b200.filtering import build_gaussian_kernel
 
-    frame = synth.config4(1024, tile=256)
+    frames = [synth.config4(1024, seed=4 + k, tile=256) for k in range(3)]
     w = build_gaussian_kernel(1.4, radius=radius).weights
-    plan = bands.band_plan(frame.shape[0], world) if world != 3 else [(0, 300), (300, 701), (701, 1024)]
-    lab, fin = canny.canny_u8(torch.from_numpy(frame).cuda(), w, 20.0, 50.0)
-    lab, fin = lab.cpu().numpy()[0], fin.cpu().numpy()[0]
+    plan = bands.band_plan(1024, world) if world != 3 else [(0, 300), (300, 701), (701, 1024)]
+    want = []
+    for f in frames:
+        lab, fin = canny.canny_u8(torch.from_numpy(f).cuda(), w, 20.0, 50.0)
+        want.append((lab.cpu().numpy()[0], fin.cpu().numpy()[0]))
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(world, _free_port(), frame, plan, w, 20.0, 50.0, 2, out), nprocs=world, join=True)
+    steps = 5
+    mp.spawn(_worker, args=(world, _free_port(), frames, plan, w, 20.0, 50.0, steps, out), nprocs=world, join=True)
     for rank, (s, e) in enumerate(plan):
-        bl, bf = out[rank]
-        assert np.array_equal(bl, lab[s:e]), rank
-        assert np.array_equal(bf, fin[s:e]), rank
+        for step in range(steps):
+            bl, bf = out[rank][step]
+            lab, fin = want[step % len(frames)]
+            assert np.array_equal(bl, lab[s:e]), (rank, step)
+            assert np.array_equal(bf, fin[s:e]), (rank, step)
+
+
+def test_stream_flags_order_work():
+    """ef_stream_write_u32 / ef_stream_wait_u32: a stream blocked on a flag
+    runs its later work only after another stream publishes the value."""
+    from paper_1710_07745_b200 import _lib, canny
+
+    canny.require_cuda()
+    lib = _lib.load()
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    x = torch.zeros(1 << 20, device="cuda")
+    y = torch.empty_like(x)  # allocated up front: a cudaMalloc now would wait for the blocked stream
+    torch.cuda.synchronize()
+    _lib.check(lib.ef_stream_wait_u32(flag.data_ptr(), 7, b.cuda_stream), "wait")
+    with torch.cuda.stream(b):
+        torch.add(x, 1.0, out=y)  # queued behind the wait
+    with torch.cuda.stream(a):
+        x.fill_(41.0)
+    _lib.check(lib.ef_stream_write_u32(flag.data_ptr(), 7, a.cuda_stream), "write")
+    torch.cuda.synchronize()
+    assert float(y[0]) == 42.0 and int(flag[0]) == 7
+    with pytest.raises(ValueError):
+        _lib.check(lib.ef_stream_write_u32(flag.data_ptr() + 2, 1, a.cuda_stream), "write")
 
 
 def test_peer_abi_validation():
