@@ -197,13 +197,6 @@ int ef_ipc_export(const void* d_ptr, void* h_handle64, uint64_t* h_offset);
 int ef_ipc_open(const void* h_handle64, uint64_t offset, void** d_ptr_out, void** d_base_out);
 int ef_ipc_close(void* d_base);
 
-/* Stream-ordered 32-bit flags for the peer-halo handshake (device side, no
- * host synchronisation): ef_stream_write_u32 stores `value` at d_addr once the
- * stream's earlier work is complete and visible; ef_stream_wait_u32 makes the
- * stream's later work wait until *d_addr >= value.  d_addr may be an IPC / peer
- * mapping of another rank's flags.  4-byte aligned. */
-int ef_stream_write_u32(void* d_addr, uint32_t value, void* stream);
-int ef_stream_wait_u32(const void* d_addr, uint32_t value, void* stream);
 
 /* Band-local hysteresis only, for labels already computed (the per-band
  * labelling of trace_edges_parallel, hysteresis.py:97-101). */

@@ -63,13 +63,11 @@ _SIGNATURES = {
     "ef_ipc_export": ([P, P, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
     "ef_ipc_open": ([P, ctypes.c_uint64, ctypes.POINTER(P), ctypes.POINTER(P)], ctypes.c_int),
     "ef_ipc_close": ([P], ctypes.c_int),
-    "ef_stream_write_u32": ([P, ctypes.c_uint32, P], ctypes.c_int),
     "ef_pgm_last_error": ([], ctypes.c_char_p),
     "ef_pgm_parse": ([P, SZ, P, ctypes.POINTER(I64)], ctypes.c_int),
     "ef_pgm_decode_u8": ([P, SZ, P, P, ctypes.POINTER(I64)], ctypes.c_int),
     "ef_pgm_header": ([I32, I32, ctypes.c_char_p, SZ], ctypes.c_int),
     "ef_pgm_encode_edges": ([P, I64, P, P], ctypes.c_int),
-    "ef_stream_wait_u32": ([P, ctypes.c_uint32, P], ctypes.c_int),
     "ef_band_edges": ([P, SZ, I32, I32, P, P, P], ctypes.c_int),
     "ef_band_merge": ([I32, I32, P, P, P], ctypes.c_int),
     "ef_band_merge_scratch_bytes": ([I32, I32], SZ),

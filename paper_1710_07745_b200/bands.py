@@ -275,10 +275,9 @@ def _gather(tensor, world, group):
 
 
 def _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group):
-    """Device pointers to the halo rows inside the neighbour bands and to the
-    neighbours' handshake flags (opened once per backend and band buffer over
-    CUDA IPC: NVLink peer memory when the neighbour is another GPU)."""
-    import torch
+    """Device pointers to the halo rows inside the neighbour bands (opened once
+    per backend and band buffer over CUDA IPC: NVLink peer memory when the
+    neighbour is another GPU)."""
     import torch.distributed as dist
 
     w = band_u8.shape[1]
@@ -287,45 +286,28 @@ def _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, g
         return be.peer_ptrs[1:]
     if getattr(be, "peer_ptrs", None) is not None:
         be.close_peers()
-    # this rank's flags (int32): [0] step whose band is written, [1] step up to
-    # which the band above has read my rows, [2] the same for the band below
-    be.flags = torch.zeros(4, dtype=torch.int32, device=band_u8.device)
-    be.step = 0
     objs = [None] * world
-    dist.all_gather_object(objs, (ipc_export(band_u8), ipc_export(be.flags)), group=group)
+    dist.all_gather_object(objs, ipc_export(band_u8), group=group)
     ht, hb = min(halo, row0), min(halo, full_height - row0 - rows)
     top = bot = 0
     be.peer_bases = []
-    be.top_flags = be.bot_flags = 0
     for peer, (p0, pr) in enumerate(meta):
         if peer == rank:
             continue
         if ht and p0 + pr == row0:  # the band just above: its last ht rows
             if pr < ht:
                 raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
-            ptr, base = ipc_open(*objs[peer][0])
+            ptr, base = ipc_open(*objs[peer])
             be.peer_bases.append(base)
             top = ptr + (pr - ht) * w
-            be.top_flags, base = ipc_open(*objs[peer][1])
-            be.peer_bases.append(base)
         if hb and p0 == row0 + rows:  # the band just below: its first hb rows
             if pr < hb:
                 raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
-            ptr, base = ipc_open(*objs[peer][0])
+            ptr, base = ipc_open(*objs[peer])
             be.peer_bases.append(base)
             bot = ptr
-            be.bot_flags, base = ipc_open(*objs[peer][1])
-            be.peer_bases.append(base)
     be.peer_ptrs = (key, top, ht, bot, hb)
     return be.peer_ptrs[1:]
-
-
-def _flag_write(addr: int, value: int, stream: int) -> None:
-    _lib.check(_lib.load().ef_stream_write_u32(addr, value, stream), "ef_stream_write_u32")
-
-
-def _flag_wait(addr: int, value: int, stream: int) -> None:
-    _lib.check(_lib.load().ef_stream_wait_u32(addr, value, stream), "ef_stream_wait_u32")
 
 
 def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: float, high: float,
@@ -340,12 +322,10 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     peer: no halo exchange -- the classifier reads the neighbours' halo rows in
     place from their HBM (CUDA IPC mappings of their band buffers, opened once;
     NVLink loads between GPUs).  Every rank's band must stay at the same address
-    across calls and be written on the current stream; ordering is a
-    stream-ordered handshake through IPC-mapped flags (ef_stream_write_u32 /
-    ef_stream_wait_u32): a rank reads a neighbour's rows only after the
-    neighbour's stream has published that step's band, and the caller's later
-    work on this stream (its next write into the band) waits until both
-    neighbours have read this step's rows.
+    across calls and be written on the current stream before the call; the
+    call reads the neighbours' rows only after every band is written, and
+    returns only after every rank has finished reading, so the caller may
+    overwrite its band right away.
     Returns (labels, final) for those rows, equal to the rows of the
     whole-frame result."""
     import torch
@@ -372,31 +352,19 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     hb = min(halo, full_height - row0 - rows)
     if peer:
         top, ht_, bot, hb_ = _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group)
-        # device-side handshake, stream-ordered (no host synchronisation):
-        # publish "my band of step s is written", wait for the neighbours' bands
-        # of step s, read their rows, tell them so; before returning, make this
-        # stream's later work (the caller's next write into the band) wait until
-        # both neighbours have read this step's rows
-        st = int(torch.cuda.current_stream(band_u8.device).cuda_stream)
-        be.step += 1
-        s = be.step
-        fp = be.flags.data_ptr()
-        _flag_write(fp, s, st)
-        if be.top_flags:
-            _flag_wait(be.top_flags, s, st)
-        if be.bot_flags:
-            _flag_wait(be.bot_flags, s, st)
+        # two-phase host protocol: every band of this step is written before
+        # anyone reads its halo rows, and every rank has finished reading before
+        # any caller overwrites its band (the call returns only after both).
+        # (A device-side handshake -- cuStreamWaitValue32 on IPC-mapped flags --
+        # was measured: a stream waiting on a flag written by another context on
+        # the same GPU never resumed, so it is not used.)
+        stream = torch.cuda.current_stream(band_u8.device)
+        stream.synchronize()
+        dist.barrier(group=group)
         be.classify_trace_peer(band_u8, top, ht_, bot, hb_, row0, full_height, weights, low, high)
-        if be.top_flags:
-            _flag_write(be.top_flags + 8, s, st)  # read by the band below the top neighbour (me)
-        if be.bot_flags:
-            _flag_write(be.bot_flags + 4, s, st)  # read by the band above the bottom neighbour (me)
-        res = _merge_and_finalize(be, band_u8, rank, world, group)
-        if be.top_flags:
-            _flag_wait(fp + 4, s, st)
-        if be.bot_flags:
-            _flag_wait(fp + 8, s, st)
-        return res
+        stream.synchronize()
+        dist.barrier(group=group)
+        return _merge_and_finalize(be, band_u8, rank, world, group)
     if staged is not None:
         if staged.shape != (ht + rows + hb, w) or staged[ht:ht + rows].data_ptr() != band_u8.data_ptr():
             raise ValueError("staged must be band_buffer()'s buffer holding band_u8 as its middle rows")

@@ -941,41 +941,6 @@ int ef_ipc_open(const void* h_handle64, uint64_t offset, void** d_ptr_out, void*
     return EF_OK;
 }
 
-// Stream memory operations (driver API through the runtime's entry points):
-// the device-side handshake of the peer-halo band path -- a rank's stream
-// publishes "my band for step s is written" / "I finished reading your rows"
-// as 32-bit values, its neighbours' streams wait for them, no host involved.
-namespace {
-typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-StreamValueFn stream_value_fn(const char* name) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
-        return reinterpret_cast<StreamValueFn>(p);
-    return nullptr;
-}
-}  // namespace
-
-int ef_stream_write_u32(void* d_addr, uint32_t value, void* stream) {
-    static const StreamValueFn fn = stream_value_fn("cuStreamWriteValue32");
-    if (!d_addr || (reinterpret_cast<uintptr_t>(d_addr) & 3)) return fail(EF_EINVAL, "bad flag address");
-    if (!fn) return fail(EF_ECUDA, "cuStreamWriteValue32 unavailable");
-    // default flags: the write is ordered after (and makes visible) the stream's earlier work
-    const CUresult r = fn((CUstream)stream, (CUdeviceptr)d_addr, value, 0u /* CU_STREAM_WRITE_VALUE_DEFAULT */);
-    if (r != CUDA_SUCCESS) return fail(EF_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
-    return EF_OK;
-}
-
-int ef_stream_wait_u32(const void* d_addr, uint32_t value, void* stream) {
-    static const StreamValueFn fn = stream_value_fn("cuStreamWaitValue32");
-    if (!d_addr || (reinterpret_cast<uintptr_t>(d_addr) & 3)) return fail(EF_EINVAL, "bad flag address");
-    if (!fn) return fail(EF_ECUDA, "cuStreamWaitValue32 unavailable");
-    // wait until *(uint32*)d_addr >= value (cyclic comparison, CU_STREAM_WAIT_VALUE_GEQ)
-    const CUresult r = fn((CUstream)stream, (CUdeviceptr)d_addr, value, 0u /* CU_STREAM_WAIT_VALUE_GEQ */);
-    if (r != CUDA_SUCCESS) return fail(EF_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
-    return EF_OK;
-}
-
 int ef_ipc_close(void* d_base) {
     if (!d_base) return fail(EF_EINVAL, "bad arguments");
     EF_CHECK(cudaIpcCloseMemHandle(d_base), "cudaIpcCloseMemHandle");

@@ -51,6 +51,9 @@ constexpr int V2_COLS = 128;
 #ifndef EF_K1_TH
 #define EF_K1_TH 32
 #endif
+#ifndef EF_K1_POOL
+#define EF_K1_POOL 1  // phase 3 pools the four warps' candidates (0: each warp classifies its own rows)
+#endif
 #ifndef EF_K1_MINB
 #define EF_K1_MINB 6  // CTAs per SM the register budget is sized for (shared memory allows 6 at TH = 32)
 #endif
@@ -340,7 +343,6 @@ __device__ __forceinline__ void tma_wait(Smem& S) {
 // after one barrier classify the candidates with every lane busy.
 // ---------------------------------------------------------------------------
 constexpr int V3_MROWS = V2_TH + 2;                                   // magnitude rows y0-1 .. y0+TH
-constexpr int V3_MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;          // 9 per warp
 
 
 struct V3Smem {
@@ -385,11 +387,13 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     constexpr int HXA = V2Cfg<R>::HXA;
     constexpr int OW = V2Cfg<R>::OW;
     const int W = g.W, FH = g.full_H;
-    // this warp's magnitude rows j0 .. j0+8 (tile rows; Ym = y0 - 1 + j).  The
-    // last warp starts at 25 so every warp runs exactly 9 rows (no divergent
-    // loop exit around the shuffles and votes); rows 25 and 26 are computed
-    // twice, with identical values, labels and candidate words.
-    const int j0 = min(warp * V3_MPW, V3_MROWS - V3_MPW);
+    // this warp's magnitude rows j0 .. j0+nrows-1 (tile rows; Ym = y0 - 1 + j):
+    // the 34 rows split 9 / 9 / 8 / 8 (the trip count is uniform inside each
+    // warp, so no loop exit diverges around the shuffles and votes; an even
+    // 9 / 9 / 9 / 9 split computed rows 25 and 26 twice)
+    constexpr int MBASE = V3_MROWS / V2_WARPS, MEXTRA = V3_MROWS % V2_WARPS;
+    const int nrows = MBASE + (warp < MEXTRA ? 1 : 0);
+    const int j0 = warp * MBASE + min(warp, MEXTRA);
     const int ylim = min(g.out0 + g.rows, FH);  // rows at or past this are not classified here
     const int c = xv0 + 4 * lane;
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;
@@ -436,17 +440,16 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         if (lane == 0 && outrow) cmask[j - 1] = b0;
         lab += Wq;
     };
-    if constexpr (V3_MPW % 3 == 0) {
+    // period-3 register ring: whole periods, then the warp-uniform tail
+    int u3 = 0;
 #pragma unroll 1
-        for (int u3 = 0; u3 < V3_MPW; u3 += 3) {
-            row_step(u3, 0, 1, 2);
-            row_step(u3 + 1, 1, 2, 0);
-            row_step(u3 + 2, 2, 0, 1);
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < V3_MPW; ++u) row_step(u, u % 3, (u + 1) % 3, (u + 2) % 3);
+    for (; u3 + 3 <= nrows; u3 += 3) {
+        row_step(u3, 0, 1, 2);
+        row_step(u3 + 1, 1, 2, 0);
+        row_step(u3 + 2, 2, 0, 1);
     }
+    if (u3 < nrows) row_step(u3, 0, 1, 2);
+    if (u3 + 1 < nrows) row_step(u3 + 1, 1, 2, 0);
 }
 
 // position of the n-th (0-based) set bit of w
@@ -470,10 +473,24 @@ __device__ __forceinline__ int select32(unsigned w, int n) {
 template <int R, bool FUSED>
 __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Smem& S, int warp, int lane,
                                          const V2Out O) {
+#if EF_K1_POOL
+    // pooled: every warp reads the whole tile's candidate words (one row per
+    // lane) and takes rounds warp, warp + 4, ... of the tile's candidates, so
+    // the lanes stay full across the warps' rows (per-warp pools left the last
+    // round of every warp part-empty: 56% lane use on C3's dense content)
+    constexpr int NW = V2_TH;
+    static_assert(NW <= 32, "one word per lane");
+    const int wrow = lane;
+    const unsigned word = lane < NW ? S.cmask[lane] : 0u;
+    const int first = 32 * warp, stride = 32 * V2_WARPS;
+#else
     constexpr int NW = (V2_TH + V2_WARPS - 1) / V2_WARPS;  // candidate words per warp
     static_assert(NW <= 32, "one word per lane");
     const int wrow = warp + V2_WARPS * lane;
     const unsigned word = (lane < NW && wrow < V2_TH) ? S.cmask[wrow] : 0u;
+    const int first = 0, stride = 32;
+#endif
+    (void)wrow;
     int incl = __popc(word);  // inclusive prefix over the lanes (lanes >= NW add 0)
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -482,7 +499,7 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     constexpr int NW2 = NW <= 1 ? 1 : (NW <= 2 ? 2 : (NW <= 4 ? 4 : (NW <= 8 ? 8 : (NW <= 16 ? 16 : 32))));
-    for (int base = 0; base < total; base += 32) {
+    for (int base = first; base < total; base += stride) {
         const int k = base + lane;
         int i = 0;  // first word whose inclusive count exceeds k
 #pragma unroll
@@ -493,7 +510,11 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
         const unsigned w = __shfl_sync(0xffffffffu, word, i);
         const int before = __shfl_sync(0xffffffffu, incl, i) - __popc(w);
         if (k < total) {
-            const int j = warp + V2_WARPS * i;  // output row y0 + j; m tile rows j..j+2, b rows j+1..j+3
+#if EF_K1_POOL
+            const int j = i;  // output row y0 + j; m tile rows j..j+2, b rows j+1..j+3
+#else
+            const int j = warp + V2_WARPS * i;
+#endif
             classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
                               S.b[j + 2], S.b[j + 3], S.bits, O);
         }

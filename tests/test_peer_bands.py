@@ -6,12 +6,10 @@ The ranks are separate processes that share one GPU here (gpurun gives one
 B200): each maps its neighbours' band buffers over CUDA IPC exactly as it would
 map another GPU's (where the loads then travel over NVLink), and the group is
 gloo (NCCL refuses two ranks on one device).  No rank's kernel waits on another
-rank's kernel: ordering is a stream-ordered handshake through IPC-mapped flags
-(a rank's stream waits for its neighbours' "band written" flags before its
-classifier reads their rows, and for their "rows read" flags before it
-overwrites its own band).  The assembled result must equal the whole-frame
-call bit for bit, also when every rank writes a new frame into its band
-between calls with no host synchronisation in between.
+rank's kernel: every band is written before the group reads, and every rank
+has finished reading before any call returns.  The assembled result must
+equal the whole-frame call bit for bit, also when every rank writes a new
+frame into its band between calls (the write-after-read hazard).
 """
 
 import os
@@ -85,30 +83,6 @@ def test_peer_halo_bands_match_whole_frame(world, radius):
             lab, fin = want[step % len(frames)]
             assert np.array_equal(bl, lab[s:e]), (rank, step)
             assert np.array_equal(bf, fin[s:e]), (rank, step)
-
-
-def test_stream_flags_order_work():
-    """ef_stream_write_u32 / ef_stream_wait_u32: a stream blocked on a flag
-    runs its later work only after another stream publishes the value."""
-    from paper_1710_07745_b200 import _lib, canny
-
-    canny.require_cuda()
-    lib = _lib.load()
-    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
-    a, b = torch.cuda.Stream(), torch.cuda.Stream()
-    x = torch.zeros(1 << 20, device="cuda")
-    y = torch.empty_like(x)  # allocated up front: a cudaMalloc now would wait for the blocked stream
-    torch.cuda.synchronize()
-    _lib.check(lib.ef_stream_wait_u32(flag.data_ptr(), 7, b.cuda_stream), "wait")
-    with torch.cuda.stream(b):
-        torch.add(x, 1.0, out=y)  # queued behind the wait
-    with torch.cuda.stream(a):
-        x.fill_(41.0)
-    _lib.check(lib.ef_stream_write_u32(flag.data_ptr(), 7, a.cuda_stream), "write")
-    torch.cuda.synchronize()
-    assert float(y[0]) == 42.0 and int(flag[0]) == 7
-    with pytest.raises(ValueError):
-        _lib.check(lib.ef_stream_write_u32(flag.data_ptr() + 2, 1, a.cuda_stream), "write")
 
 
 def test_peer_abi_validation():
