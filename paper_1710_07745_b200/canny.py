@@ -114,6 +114,26 @@ def canny_u8(frames, weights, low: float, high: float, labels=None, final=None, 
     return labels, final
 
 
+def canny_u8_timed(frames, weights, low: float, high: float):
+    """canny_u8 on the current stream with device time per phase (CUDA events
+    the library records around the classifier and its fix-ups): returns
+    (labels, final, classify_ms, hysteresis_ms).  Synchronises."""
+    torch = require_cuda()
+    lib = _lib.load()
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(st)  # torch creates its events on first record
+    ev[1].record(st)
+    _lib.check(lib.ef_set_classify_events(ev[0].cuda_event, ev[1].cuda_event), "ef_set_classify_events")
+    try:
+        labels, final = canny_u8(frames, weights, low, high, stream=st)
+    finally:
+        _lib.check(lib.ef_set_classify_events(None, None), "ef_set_classify_events")
+    ev[2].record(st)
+    ev[2].synchronize()
+    return labels, final, ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+
+
 def classify_u8(frames, weights, low: float, high: float, labels=None, ws=None, stream=None):
     torch = require_cuda()
     x = _frames(frames, "torch.uint8")

@@ -51,6 +51,9 @@ constexpr int V2_COLS = 128;
 #ifndef EF_K1_TH
 #define EF_K1_TH 32
 #endif
+#ifndef EF_K1_MSPLIT
+#define EF_K1_MSPLIT 0  // 1: magnitude rows split 9/9/8/8 (no recomputed rows; measured 3% slower on C3)
+#endif
 #ifndef EF_K1_POOL
 #define EF_K1_POOL 1  // phase 3 pools the four warps' candidates (0: each warp classifies its own rows)
 #endif
@@ -391,9 +394,17 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     // the 34 rows split 9 / 9 / 8 / 8 (the trip count is uniform inside each
     // warp, so no loop exit diverges around the shuffles and votes; an even
     // 9 / 9 / 9 / 9 split computed rows 25 and 26 twice)
+#if EF_K1_MSPLIT
     constexpr int MBASE = V3_MROWS / V2_WARPS, MEXTRA = V3_MROWS % V2_WARPS;
     const int nrows = MBASE + (warp < MEXTRA ? 1 : 0);
     const int j0 = warp * MBASE + min(warp, MEXTRA);
+#else
+    // every warp runs ceil(34 / 4) = 9 rows; the last one starts at 25, so rows
+    // 25 and 26 are computed twice (same values, labels and candidate words)
+    constexpr int MPW = (V3_MROWS + V2_WARPS - 1) / V2_WARPS;
+    constexpr int nrows = MPW;
+    const int j0 = min(warp * MPW, V3_MROWS - MPW);
+#endif
     const int ylim = min(g.out0 + g.rows, FH);  // rows at or past this are not classified here
     const int c = xv0 + 4 * lane;
     const bool out_lane = lane >= HXA / 4 && lane < (HXA + OW) / 4 && c < W;

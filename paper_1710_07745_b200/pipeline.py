@@ -80,9 +80,13 @@ def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming]
     """blur -> sobel -> nms -> threshold -> trace (or blur -> laplacian), on the GPU.
 
     Output is bit-identical to the reference for the same inputs and config.
-    ``timings`` receives one StageTiming per device phase ("canny" for the
-    fused path, "laplacian"); ``band_times`` is accepted for signature
-    compatibility (there are no CPU bands)."""
+    ``timings`` receives the reference's five StageTiming records (bench.py:
+    76-120) with device times from CUDA events: "gaussian" carries the fused
+    classifier (blur, Sobel, NMS and thresholds run in one kernel, plus its
+    exact fix-ups), "sobel" / "nms" / "threshold" record 0 ns (fused into it),
+    "hysteresis" the tracing kernels; operator="laplacian" records "gaussian"
+    and "laplacian".  ``band_times`` is accepted for signature compatibility
+    (there are no CPU bands)."""
     from . import canny
 
     torch = canny.require_cuda()
@@ -93,17 +97,22 @@ def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming]
     px = img.pixels
     u8 = img.as_u8()
 
-    def record(stage: str, t0: int):
+    def record(stage: str, t0: int, ns: int | None = None):
         if timings is not None:
             timings.append(StageTiming(stage_name=stage, workers=cfg.workers.workers,
-                                       wall_ns=clock() - t0, rows_processed=img.height))
+                                       wall_ns=int(clock() - t0 if ns is None else ns), rows_processed=img.height))
 
     if cfg.operator == "laplacian":
-        t0 = clock()
         src = torch.from_numpy(np.ascontiguousarray(px)).cuda()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
         blurred = canny.blur_f64(src, w)
-        result.response = GrayImage.from_array(canny.laplacian_f64(blurred).cpu().numpy())
-        record("laplacian", t0)
+        ev[1].record()
+        resp = canny.laplacian_f64(blurred)
+        ev[2].record()
+        result.response = GrayImage.from_array(resp.cpu().numpy())
+        record("gaussian", 0, ev[0].elapsed_time(ev[1]) * 1e6)
+        record("laplacian", 0, ev[1].elapsed_time(ev[2]) * 1e6)
         if keep_intermediates:
             result.blurred = GrayImage.from_array(blurred.cpu().numpy())
         return result
@@ -115,7 +124,16 @@ def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming]
         dev_src = torch.from_numpy(u8 if u8 is not None else np.ascontiguousarray(px)).cuda()
     if thresholds is None:
         thresholds = _auto_from_peak(canny.thinned_max(dev_src, w))
-    if u8 is not None and cfg.hysteresis_mode == "serial":
+    stage_ms = None
+    if u8 is not None and cfg.hysteresis_mode == "serial" and timings is not None:
+        # device-resident call with per-phase events (the host-buffer path
+        # pipelines several chunks on internal streams)
+        if dev_src is None:
+            dev_src = torch.from_numpy(u8).cuda()
+        lab_d, fin_d, c_ms, h_ms = canny.canny_u8_timed(dev_src, w, thresholds.low, thresholds.high)
+        labels, final = lab_d[0].cpu().numpy(), fin_d[0].cpu().numpy()
+        stage_ms = (c_ms, h_ms)
+    elif u8 is not None and cfg.hysteresis_mode == "serial":
         labels, final = canny.canny_u8_host(u8, w, thresholds.low, thresholds.high)
     else:
         if dev_src is None:
@@ -132,7 +150,13 @@ def run_pipeline(img: GrayImage, cfg: PipelineConfig, timings: list[StageTiming]
         else:
             fin_d = canny.trace_edges_u8(lab_d)[0]
         labels, final = lab_d.cpu().numpy(), fin_d.cpu().numpy()
-    record("canny", t0)
+    if timings is not None:
+        if stage_ms is None:  # exact / parallel paths: the whole call as the fused stage
+            stage_ms = ((clock() - t0) / 1e6, 0.0)
+        record("gaussian", t0, stage_ms[0] * 1e6)
+        for fused in ("sobel", "nms", "threshold"):
+            record(fused, t0, 0)
+        record("hysteresis", t0, stage_ms[1] * 1e6)
     edges = EdgeMap(width=img.width, height=img.height, labels=np.ascontiguousarray(labels),
                     final=np.ascontiguousarray(final).view(np.bool_))
     result.edges = edges

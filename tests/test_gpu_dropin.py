@@ -168,3 +168,21 @@ def test_detect_pgm_matches_reference_cli_bytes(ef):
         assert ef.save_pgm(ef.edges_to_image(res.edges)) == want, key
     with pytest.raises(ef.PgmFormatError):
         ef.detect_pgm(b"P5 2 2 255 \x00", cfgs["t2050"])
+
+
+def test_run_pipeline_stage_timings(ef):
+    """timings receives the reference's five stage records (bench.py:76-120)
+    with device times; results are unchanged by timing."""
+    g = load("pipeline.npz")
+    name = [str(n) for n in g["names"]][-1]
+    arr = g[f"{name}/input"]
+    timings = []
+    res = ef.run_pipeline(ef.GrayImage.from_array(arr), ef.PipelineConfig(sigma=1.4, thresholds=ef.Thresholds(20.0, 50.0)),
+                          timings=timings)
+    assert [t.stage_name for t in timings] == ["gaussian", "sobel", "nms", "threshold", "hysteresis"]
+    assert timings[0].wall_ns > 0 and timings[4].wall_ns > 0 and all(t.rows_processed == arr.shape[0] for t in timings)
+    assert np.array_equal(res.edges.labels, g[f"{name}/t2050/labels"])
+    assert np.array_equal(res.edges.final, unpack(g[f"{name}/t2050/final"], arr.shape))
+    t2 = []
+    ef.run_pipeline(ef.GrayImage.from_array(arr), ef.PipelineConfig(operator="laplacian"), timings=t2)
+    assert [t.stage_name for t in t2] == ["gaussian", "laplacian"]
