@@ -349,15 +349,30 @@ int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const
     return EF_OK;
 }
 
-// reset: the workspace header has not been initialised by a classify launch of
-// this call (standalone tracing).
+// The workspace's foreground bit planes for frames of H rows x W columns.
+FgBits ws_planes(const Ws& ws, int H, int W) {
+    const int words = (W + 63) / 64;
+    return FgBits{ws.fgbits, ws.stbits, words, (unsigned long long)H * words, 0};
+}
+
+// Hysteresis over the bit planes: the classifier's (bits, with final = strong
+// already written) or, without them, planes packed from the label bytes plus
+// final = strong.  reset: the workspace header has not been initialised by a
+// classify launch of this call (standalone tracing).
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
               cudaStream_t st, bool finalize, bool reset, const FgBits* bits = nullptr) {
     const int sms = sm_count_current();
     if (reset) EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");
-    if (bits && !bits->fg) bits = nullptr;
-    EF_CHECK(launch_hyst_local(labels, batch, H, W, fin, ws.hb, ws.hdr, bits, sms, st), "hysteresis");
-    if (finalize) EF_CHECK(launch_hyst_final(labels, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
+    FgBits B;
+    if (bits && bits->fg) {
+        B = *bits;
+    } else {
+        B = ws_planes(ws, H, W);
+        EF_CHECK(launch_hyst_pack(labels, batch, H, W, B, sms, st), "bit-plane pack");
+        EF_CHECK(launch_strong_final(labels, (long long)batch * H * W, fin, sms, st), "final = strong");
+    }
+    EF_CHECK(launch_hyst_local(B, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis");
+    if (finalize) EF_CHECK(launch_hyst_final(B, batch, H, W, fin, ws.hb, ws.hdr, sms, st), "hysteresis finalize");
     return EF_OK;
 }
 
@@ -966,7 +981,8 @@ int ef_band_edges(const void* d_workspace, size_t workspace_bytes, int32_t rows,
     if ((rc = check_ws(const_cast<void*>(d_workspace), workspace_bytes, L))) return rc;
     if (!d_ids || !d_strong) return fail(EF_EINVAL, "NULL buffer");
     Ws ws = ws_bind(const_cast<void*>(d_workspace), L);
-    EF_CHECK(launch_band_edges(rows, width, ws.hb, d_ids, d_strong, (cudaStream_t)stream), "band edges");
+    EF_CHECK(launch_band_edges(rows, width, ws.hb, ws_planes(ws, rows, width), d_ids, d_strong, (cudaStream_t)stream),
+             "band edges");
     return EF_OK;
 }
 
@@ -996,7 +1012,8 @@ int ef_band_finalize(const uint8_t* d_strong_edges, int32_t rows, int32_t width,
     Ws ws = ws_bind(d_workspace, L);
     cudaStream_t st = (cudaStream_t)stream;
     EF_CHECK(launch_band_apply(rows, width, ws.hb, d_strong_edges, st), "band apply");
-    EF_CHECK(launch_hyst_final(d_labels, 1, rows, width, d_final, ws.hb, ws.hdr, sm_count_current(), st),
+    EF_CHECK(launch_hyst_final(ws_planes(ws, rows, width), 1, rows, width, d_final, ws.hb, ws.hdr, sm_count_current(),
+                               st),
              "hysteresis finalize");
     return EF_OK;
 }

@@ -10,6 +10,7 @@
 //    exact one.  Used by the fused classify kernel on u8 inputs.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/edgeforge_b200.h"
@@ -18,6 +19,23 @@ namespace ef {
 
 constexpr int kMaxR = EF_MAX_RADIUS;
 constexpr uint8_t kFlag = 0x80;  // label byte marker: decision not certified yet
+
+// Debug build (-DEF_DEBUG_CHECKS, tools/gpu_debug_checks.sh): device-side bounds
+// assertions on the shared-memory and global indices of the kernels, the
+// substitute for compute-sanitizer, which is closed on this GPU pool.  A failed
+// check traps the kernel (the call returns EF_ECUDA).  Compiled out otherwise.
+#ifdef EF_DEBUG_CHECKS
+#define EF_DCHECK(cond)                                                                           \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("EF_DCHECK failed: %s (%s:%d) block (%d,%d,%d) thread %d\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x); \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define EF_DCHECK(cond) ((void)0)
+#endif
 
 // Reference label values (hysteresis.py:19-21).
 constexpr uint8_t kNone = 0, kWeak = 1, kStrong = 2;

@@ -242,6 +242,7 @@ __device__ __forceinline__ void out_coords(unsigned long long idx, const FrameGe
     int yo = (int)(rem / g.W);
     x = (int)(rem - (unsigned long long)yo * g.W);
     y = g.out0 + yo;
+    EF_DCHECK(yo >= 0 && yo < g.rows && x >= 0 && x < g.W);
 }
 
 // the fused pipeline's foreground bit planes for a fixed pixel

@@ -75,6 +75,9 @@ struct V2Out {
     unsigned long long out_base;
     unsigned long long* fix_list;
     WsHeader* hdr;
+#ifdef EF_DEBUG_CHECKS
+    unsigned long long npx;  // pixels of the label buffer (bounds checks)
+#endif
 };
 
 template <int R>
@@ -120,6 +123,8 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
     constexpr int NR = V2Cfg<R>::NR;
     const int ys = y0 - 2 + warp * V2_P1_ROWS;
     auto fetch = [&](int Y) -> uint32_t {  // 4 staged input bytes of frame row Y
+        EF_DCHECK(Y - (y0 - 2 - R) >= 0 && Y - (y0 - 2 - R) < V2_BROWS + 2 * R);
+        EF_DCHECK((xv0 & 15) + 4 * lane + 3 < V2_IN_COLS);
         return *reinterpret_cast<const uint32_t*>(&S.in[Y - (y0 - 2 - R)][(xv0 & 15) + 4 * lane]);
     };
     float2 wf2[R + 1];
@@ -139,7 +144,8 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
 #pragma unroll
     for (int ii = 0; ii < 2 * R; ++ii) cvt(fetch(ys - R + ii), p[ii][0], p[ii][1]);
 #pragma unroll
-    for (int ii = 2 * R; ii < 4 * R; ++ii) raw[ii % NR] = fetch(ys - R + ii);
+    for (int ii = 2 * R; ii < 4 * R; ++ii)  // look-ahead rows this warp will use (R > 4: fewer than 2R)
+        if (ii - 2 * R < V2_P1_ROWS) raw[ii % NR] = fetch(ys - R + ii);
     const int rb = ys - (y0 - 2);  // first b row of this warp
 
 #pragma unroll
@@ -191,6 +197,7 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
                 b23.y = fmaf(wf2[o].x, e[11 - o] + e[11 + o], b23.y);
             }
         }
+        EF_DCHECK(rb + u >= 0 && rb + u < V2_BROWS);
         *reinterpret_cast<float4*>(&S.b[rb + u][4 * lane]) = make_float4(b01.x, b01.y, b23.x, b23.y);
     }
 }
@@ -288,6 +295,10 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
             ++slot;
         }
     }
+    EF_DCHECK(cc0 >= 4 && cc0 + 4 < V2_CS && xv0 + cc0 >= 0 && xv0 + cc0 + 4 <= P.W);
+#ifdef EF_DEBUG_CHECKS
+    EF_DCHECK(rowbase + xv0 + cc0 + 4 <= O.npx);
+#endif
     st_global_u32(O.labels + rowbase + xv0 + cc0, packed);
     if (FUSED) {
         // final = strong (kFlag bytes give 0: the fix-up writes them)
@@ -411,7 +422,10 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
     const uint32_t fill = (uint32_t)P.cls0 * 0x01010101u;
     const float cand_sq = P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f;
     const int Wq = W >> 2;
-    auto brow = [&](int Y) -> const float* { return &S.b[Y - (y0 - 2)][4 * lane]; };
+    auto brow = [&](int Y) -> const float* {
+        EF_DCHECK(Y - (y0 - 2) >= 0 && Y - (y0 - 2) <= V2_BROWS);
+        return &S.b[Y - (y0 - 2)][4 * lane];
+    };
     uint32_t* lab = reinterpret_cast<uint32_t*>(O.labels + O.out_base + (long long)(y0 + j0 - 1 - g.out0) * W + c);
     const long long fin_off = FUSED ? S.bits.fin_off : 0;  // fused path: final = 0 off the candidates
     unsigned* const cmask = S.cmask;
@@ -436,6 +450,7 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const float2 gy23 = add2(f2(sm[pd][2], sm[pd][3]), f2(-sm[pu][2], -sm[pu][3]));
         float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
         float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
+        EF_DCHECK(j >= 0 && j < V3_MROWS);
         *reinterpret_cast<float4*>(&S.m[j][4 * lane]) = make_float4(m01.x, m01.y, m23.x, m23.y);
         // output rows: groups certainly below `low` get the background class
         // now, the others are marked for the classifier
@@ -446,8 +461,12 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const bool cand = act && fmaxf(fmaxf(m01.x, m01.y), fmaxf(m23.x, m23.y)) >= cand_sq;
         const unsigned b0 = __ballot_sync(0xffffffffu, cand);
         const bool bg = act && !cand;
+        EF_DCHECK(!bg || (reinterpret_cast<const uint8_t*>(lab) >= O.labels &&
+                          reinterpret_cast<const uint8_t*>(lab) + 4 <=
+                              O.labels + (unsigned long long)gridDim.z * g.rows * g.W));
         if (bg) *lab = fill;
         if (FUSED && bg) *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lab) + fin_off) = 0u;
+        EF_DCHECK(!(lane == 0 && outrow) || (j - 1 >= 0 && j - 1 < V2_TH));
         if (lane == 0 && outrow) cmask[j - 1] = b0;
         lab += Wq;
     };
@@ -526,6 +545,8 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
 #else
             const int j = warp + V2_WARPS * i;
 #endif
+            EF_DCHECK(j >= 0 && j + 2 < V3_MROWS && j + 3 < V2_BROWS && i >= 0 && i < NW);
+            EF_DCHECK(select32(w, k - before) >= 0 && select32(w, k - before) < 32 && ((w >> select32(w, k - before)) & 1u));
             classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
                               S.b[j + 2], S.b[j + 3], S.bits, O);
         }
@@ -579,7 +600,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (tma_tile && threadIdx.x == 0) tma_issue<R, PEER>(S, tmap, xv0, y0, g);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* img = src + (size_t)blockIdx.z * g.H * g.W;
+#ifdef EF_DEBUG_CHECKS
+    const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr,
+                  (unsigned long long)gridDim.z * g.rows * g.W};
+#else
     const V2Out O{labels, (unsigned long long)blockIdx.z * g.rows * g.W, fix_list, hdr};
+#endif
     if (threadIdx.x == 0) S.bits = B;
     const bool interior = xv0 >= 0 && xv0 + V2_COLS <= g.W && y0 - 2 - R >= max(g.g0, 0) &&
                           y0 + V2_TH + 2 + R <= min(g.full_H, g.g0 + g.H) && y0 + V2_TH <= g.out0 + g.rows;

@@ -2,24 +2,35 @@
 //
 // The reference labels 8-connected components of labels != 0 with
 // scipy.ndimage.label and keeps those that contain a strong pixel.  The result
-// is a set, so any correct connected-component algorithm is bit-exact.  Here:
+// is a set, so any correct connected-component algorithm is bit-exact.  Here
+// only the WEAK pixels are labelled: a weak pixel is final iff its component
+// among the weak pixels alone touches (8-adjacency) a strong pixel.  (A path
+// from a weak pixel to a strong one runs through weak pixels up to the first
+// strong pixel it meets; conversely a weak component next to a strong pixel is
+// part of that pixel's component.)  Strong pixels are final as they stand (the
+// final map is prefilled with them), and a tile reads its neighbours' strong
+// bits at its border, so strong pixels never enter the union-find and never
+// become border nodes -- on Canny maps half or more of the foreground is
+// strong (C3: 52%, C1: 88%).  Input is the two foreground bit planes (label !=
+// 0, label == 2); callers with label bytes pack them first (hyst_pack_kernel).
 //
-//  H1 hyst_local   one CTA per 64x64 tile: lock-free union-find in shared
-//                  memory over the tile's pixels.  Components that do not touch
-//                  the tile border are final right away (kept iff they hold a
-//                  strong pixel).  Border-touching components become global
-//                  nodes, numbered tile*256 + (smallest perimeter slot).
+//  H1 hyst_local   per 64x64 tile (one warp, or a 128-thread block for dense
+//                  tiles / few-tile launches): union-find over the tile's weak
+//                  pixels in shared memory; a component is strong if any of
+//                  its pixels is next to a strong pixel of the tile or of a
+//                  neighbour tile.  Components that do not touch the tile
+//                  border are final right away; border-touching ones become
+//                  global nodes, numbered tile*256 + (smallest perimeter slot).
 //  H2 hyst_merge   unions nodes across tile seams (right, bottom, and the two
 //                  diagonal corners) with an atomicCAS union-find in HBM.
 //  H3 hyst_resolve propagates "holds a strong pixel" to every node's root.
-//  H4 hyst_final   re-runs the tile CCL only for tiles with undecided
-//                  border components and reads their roots' strong flag.
+//  H4 hyst_final   pending weak pixels read their root's strong flag (or the
+//                  pending tiles re-run the same tile CCL after an overflow).
 //
-// HBM traffic: labels read once (twice for the few pending tiles), final
-// written once, plus 9 bytes per perimeter slot (~0.5 B/pixel worst case).
 // The same machinery runs per row band for the multi-GPU partition
 // (trace_edges_parallel, hysteresis.py:90-131): band-edge components stay
-// pending until the cross-band merge.
+// pending until the cross-band merge, and strong pixels on a band's edge rows
+// are exported to it as strong singletons (read from the strong plane).
 #include <algorithm>
 
 #include "ef_common.cuh"
@@ -37,15 +48,16 @@ constexpr int LCAP = 256;           // listed foreground pixels per warp (16 row
 constexpr unsigned NO_SLOT = 0x1ffu;  // info[] slot field: component touches no perimeter slot
 
 struct TileCCL {
-    unsigned long long fgrow[HT];  // foreground (label != 0) bit per pixel, one word per row
-    unsigned long long strow[HT];  // strong bit per pixel
+    unsigned long long fgrow[HT];  // weak pixels (the union-find's foreground), one word per row
+    unsigned long long strow[HT];  // weak pixels next to a strong pixel (component seeds)
+    unsigned long long st0[HT];    // strong pixels
     unsigned short par[HT * HT];   // union-find parent; initialised for foreground pixels only
     // per root: bit 15 clear = component holds a strong pixel, bits 0..8 = its
     // smallest perimeter slot (NO_SLOT if interior); 0xffff initially
     unsigned short info[HT * HT];
     unsigned short list[H_THREADS / 32][LCAP];  // each warp's foreground pixels (lane-balanced loops)
     int wcount[H_THREADS / 32];
-    int flags;  // 1: any foreground, 2: any weak pixel, 4: a warp list overflowed
+    int flags;  // 1: any weak pixel, 2: any strong pixel, 4: a warp list overflowed
     int pending;
 };
 
@@ -181,37 +193,66 @@ __device__ __forceinline__ void pack4(uint32_t w, uint32_t& fg, uint32_t& st) {
     st = (sg * 0x10204080u) >> 28;
 }
 
-// Load this thread's 32 label bytes as foreground / strong bit masks and publish
-// the tile's row words and flags.  Also initialises union-find state for its
-// foreground pixels (runs inside the 32-pixel segment pre-linked to their
-// start) and appends them to the warp's pixel list.  The caller's barrier
-// makes everything visible.
-__device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, int H, int W, const TileGeo& g,
-                                          TileCCL& s, uint32_t& fg, uint32_t& st) {
+// One word of a foreground bit plane; 0 outside the frame (or band) rows and words.
+__device__ __forceinline__ unsigned long long plane_word(const unsigned long long* __restrict__ plane,
+                                                         const FgBits& B, int f, int Y, int rows, int j) {
+    return (Y >= 0 && Y < rows && j >= 0 && j < B.words)
+               ? __ldg(plane + (unsigned long long)f * B.frame_words + (unsigned long long)Y * B.words + j)
+               : 0ull;
+}
+
+// Edge bits of the neighbouring words that row Y's weak pixels at columns 0
+// and 63 can touch: bit 63 of word j-1 (rows Y-1..Y+1) at bit 0, bit 0 of word
+// j+1 at bit 63.  Loaded only where such a weak pixel exists (rare).
+__device__ __forceinline__ unsigned long long side_strong(const FgBits& B, int f, int Y, int rows, int j,
+                                                          unsigned long long wk) {
+    unsigned long long s = 0;
+    if (wk & 1ull) {
+        const unsigned long long l = plane_word(B.st, B, f, Y - 1, rows, j - 1) |
+                                     plane_word(B.st, B, f, Y, rows, j - 1) |
+                                     plane_word(B.st, B, f, Y + 1, rows, j - 1);
+        s |= l >> 63;
+    }
+    if (wk >> 63) {
+        const unsigned long long r = plane_word(B.st, B, f, Y - 1, rows, j + 1) |
+                                     plane_word(B.st, B, f, Y, rows, j + 1) |
+                                     plane_word(B.st, B, f, Y + 1, rows, j + 1);
+        s |= r << 63;
+    }
+    return s;
+}
+
+// Weak pixels of row Y, word j, and those of them 8-adjacent to a strong pixel
+// (the strong plane's rows Y-1..Y+1 dilated by one column, with the edge bits
+// of the neighbouring words: another tile's pixels).  Also the strong word.
+__device__ __forceinline__ void weak_row(const FgBits& B, int f, int Y, int rows, int j, unsigned long long& wk,
+                                         unsigned long long& seed, unsigned long long& st) {
+    st = plane_word(B.st, B, f, Y, rows, j);
+    wk = plane_word(B.fg, B, f, Y, rows, j) & ~st;
+    seed = 0;
+    if (wk) {
+        const unsigned long long v =
+            st | plane_word(B.st, B, f, Y - 1, rows, j) | plane_word(B.st, B, f, Y + 1, rows, j);
+        seed = wk & (v | (v << 1) | (v >> 1) | side_strong(B, f, Y, rows, j, wk));
+    }
+}
+
+// Load this thread's 32-pixel row segment from the bit planes (weak pixels,
+// their strong-adjacent seeds, the strong pixels) and publish the tile's row
+// words and flags.  Also initialises union-find state for its weak pixels
+// (runs inside the 32-pixel segment pre-linked to their start) and appends
+// them to the warp's pixel list.  The caller's barrier makes everything visible.
+__device__ __forceinline__ void tile_load(const FgBits& B, int rows, const TileGeo& g, TileCCL& s, uint32_t& fg,
+                                          uint32_t& st) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int row = tid >> 1, seg = (tid & 1) * 32;
-    const uint8_t* src = labels + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
-    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    if (row < g.vh && seg + 32 <= g.vw && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
-        const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + 16));
-        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-    } else if (row < g.vh && seg < g.vw) {
-        const int n = min(32, g.vw - seg);
-        for (int k = 0; k < n; ++k) w[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
-    }
-    fg = 0;
-    st = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        uint32_t f, t;
-        pack4(w[j], f, t);
-        fg |= f << (4 * j);
-        st |= t << (4 * j);
-    }
+    unsigned long long wk = 0, seed = 0, strong = 0;
+    if (row < g.vh) weak_row(B, g.f, g.y0 + row, rows, g.txi, wk, seed, strong);
+    fg = (uint32_t)(wk >> seg);
+    st = (uint32_t)(seed >> seg);
     reinterpret_cast<uint32_t*>(&s.fgrow[row])[tid & 1] = fg;
     reinterpret_cast<uint32_t*>(&s.strow[row])[tid & 1] = st;
+    reinterpret_cast<uint32_t*>(&s.st0[row])[tid & 1] = (uint32_t)(strong >> seg);
     // warp-exclusive prefix of the foreground counts -> list positions
     const int cnt = __popc(fg);
     int off = cnt;
@@ -234,11 +275,11 @@ __device__ __forceinline__ void tile_load(const uint8_t* __restrict__ labels, in
         s.info[i] = 0xffffu;
         if (listed) s.list[warp][off++] = (unsigned short)i;
     }
-    const unsigned any_fg = __any_sync(0xffffffffu, fg != 0);
-    const unsigned any_weak = __any_sync(0xffffffffu, (fg & ~st) != 0);
+    const unsigned any_weak = __any_sync(0xffffffffu, fg != 0);
+    const unsigned any_strong = __any_sync(0xffffffffu, (uint32_t)(strong >> seg) != 0u);
     if (lane == 0) {
         s.wcount[warp] = total;
-        const int f = (any_fg ? 1 : 0) | (any_weak ? 2 : 0) | (listed ? 0 : 4);
+        const int f = (any_weak ? 1 : 0) | (any_strong ? 2 : 0) | (listed ? 0 : 4);
         if (f) atomicOr(&s.flags, f);
     }
 }
@@ -346,24 +387,10 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
     __syncthreads();
 }
 
-// 32 bits -> 32 bytes (0/1)
-__device__ __forceinline__ void store32(uint8_t* dst, int valid, uint32_t bits) {
-    uint32_t o[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = (((bits >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u;
-    if (valid >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
-    } else {
-        for (int k = 0; k < valid && k < 32; ++k) dst[k] = (uint8_t)(o[k >> 2] >> (8 * (k & 3)));
-    }
-}
-
-// H1: tile-local hysteresis.  Empty tiles write zeros; tiles whose foreground
-// is all strong are final as they stand and export every border pixel as its
-// own strong node (no union-find: anything touching them is strong anyway);
-// other tiles run the shared-memory union-find and append the pixels of
-// undecided border components to the pending list for H4.
+// H1: tile-local hysteresis.  Tiles without weak pixels are final as they
+// stand (the final map holds their strong pixels) and export nothing; other
+// tiles run the shared-memory union-find over their weak pixels and append the
+// pixels of undecided border components to the pending list for H4.
 // one border-component node into the node list stripe of its tile
 __device__ __forceinline__ void append_node(const HystBufs& b, WsHeader* hdr, long long tile, int node) {
     const int stripe = (int)(tile % PL_STRIPES);
@@ -372,78 +399,71 @@ __device__ __forceinline__ void append_node(const HystBufs& b, WsHeader* hdr, lo
     else hdr->node_overflow = 1u;
 }
 
-__device__ __forceinline__ void hyst_block_tile(const uint8_t* __restrict__ labels, int H, int W,
-                                                uint8_t* __restrict__ final_out, const HystBufs& b, WsHeader* hdr,
-                                                long long tile, const TileGeo& g, TileCCL& s) {
+__device__ __forceinline__ void hyst_block_tile(const FgBits& B, int H, int W, uint8_t* __restrict__ final_out,
+                                                const HystBufs& b, WsHeader* hdr, long long tile, const TileGeo& g,
+                                                TileCCL& s) {
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
     if (tid == 0) { s.pending = 0; s.flags = 0; }
     __syncthreads();
-    uint32_t fg, st;
-    tile_load(labels, H, W, g, s, fg, st);
+    uint32_t fg, st;  // this thread's weak pixels and their strong-adjacent seeds
+    tile_load(B, H, g, s, fg, st);
     __syncthreads();
     const int flags = s.flags;
-    const int kind = (flags & 1) ? ((flags & 2) ? 2 : 1) : 0;  // 0 empty, 1 strong-only, 2 general
-    uint32_t fin = 0;
-    if (kind) {
-        if (kind == 1) {
-            fin = fg;
-        } else {
-            tile_ccl(g, s, fg, st, !(flags & 4));
-            uint32_t pend = 0;
-            uint32_t m = fg;
-            while (m) {
-                const int k = __ffs(m) - 1;
-                m &= m - 1;
-                const unsigned v = s.info[s.par[row * HT + seg + k]];
-                if (info_strong(v)) fin |= 1u << k;
-                else if (info_slot(v) != NO_SLOT) pend |= 1u << k;
-            }
-            if (pend) {
-                s.pending = 1;
-                const int cnt = __popc(pend);
-                const int stripe = (int)(tile % PL_STRIPES);
-                unsigned long long at = atomicAdd(&b.plist_count[stripe], (unsigned long long)cnt);
-                if (at + cnt > b.plist_scap) {
-                    hdr->plist_overflow = 1u;
-                } else {
-                    at += (unsigned long long)stripe * b.plist_scap;
-                    const unsigned long long base =
-                        (unsigned long long)g.f * H * W + (unsigned long long)(g.y0 + row) * W + g.x0 + seg;
-                    int j = 0;
-                    while (pend) {
-                        const int k = __ffs(pend) - 1;
-                        pend &= pend - 1;
-                        const int root = s.par[row * HT + seg + k];
-                        b.plist_idx[at + j] = base + k;
-                        b.plist_node[at + j] = (int)(tile * HP) + (int)info_slot(s.info[root]);
-                        ++j;
-                    }
+    const bool general = flags & 1;  // any weak pixel (else the tile is final as it stands)
+    if (general) {
+        tile_ccl(g, s, fg, st, !(flags & 4));
+        uint32_t fin = 0, pend = 0;
+        uint32_t m = fg;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const unsigned v = s.info[s.par[row * HT + seg + k]];
+            if (info_strong(v)) fin |= 1u << k;
+            else if (info_slot(v) != NO_SLOT) pend |= 1u << k;
+        }
+        if (pend) {
+            s.pending = 1;
+            const int cnt = __popc(pend);
+            const int stripe = (int)(tile % PL_STRIPES);
+            unsigned long long at = atomicAdd(&b.plist_count[stripe], (unsigned long long)cnt);
+            if (at + cnt > b.plist_scap) {
+                hdr->plist_overflow = 1u;
+            } else {
+                at += (unsigned long long)stripe * b.plist_scap;
+                const unsigned long long base =
+                    (unsigned long long)g.f * H * W + (unsigned long long)(g.y0 + row) * W + g.x0 + seg;
+                int j = 0;
+                while (pend) {
+                    const int k = __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    const int root = s.par[row * HT + seg + k];
+                    b.plist_idx[at + j] = base + k;
+                    b.plist_node[at + j] = (int)(tile * HP) + (int)info_slot(s.info[root]);
+                    ++j;
                 }
             }
         }
+        // weak pixels that join an edge (the final map holds the strong pixels)
+        uint8_t* dst = final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg;
+        while (fin) {
+            const int k = __ffs(fin) - 1;
+            fin &= fin - 1;
+            EF_DCHECK(row < g.vh && seg + k < g.vw);
+            dst[k] = 1;
+        }
     }
-    if (row < g.vh && seg < g.vw)
-        store32(final_out + (size_t)g.f * H * W + (size_t)(g.y0 + row) * W + g.x0 + seg, g.vw - seg, fin);
-    // perimeter slots p = tid and tid + 128: node id of the component at the slot
+    // perimeter slots p = tid and tid + 128: node id of the weak component at the slot
     int any_node = 0;
+    if (general) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int p = tid + h * H_THREADS;
-        int y, x;
-        slot_pixel(p, g.vh, g.vw, y, x);
-        int node = -1;
-        const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
-        if (kind && valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
-            if (kind == 1) {
-                const int own = perim_slot(y, x, g.vh, g.vw);
-                node = (int)(tile * HP) + own;
-                if (own == p) {
-                    b.gpar[node] = node;
-                    b.gstrong[node] = 1;
-                    append_node(b, hdr, tile, node);
-                }
-            } else {
+        for (int h = 0; h < 2; ++h) {
+            const int p = tid + h * H_THREADS;
+            int y, x;
+            slot_pixel(p, g.vh, g.vw, y, x);
+            int node = -1;
+            const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
+            if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
                 const unsigned v = s.info[s.par[y * HT + x]];
                 node = (int)(tile * HP) + (int)info_slot(v);
                 if (info_slot(v) == (unsigned)p) {
@@ -452,9 +472,9 @@ __device__ __forceinline__ void hyst_block_tile(const uint8_t* __restrict__ labe
                     append_node(b, hdr, tile, node);
                 }
             }
+            b.perim[tile * HP + p] = node;
+            any_node |= node >= 0;
         }
-        b.perim[tile * HP + p] = node;
-        any_node |= node >= 0;
     }
     any_node = __syncthreads_or(any_node);
     if (tid == 0) {
@@ -474,15 +494,15 @@ __device__ __forceinline__ TileGeo tile_geo_linear(long long tile, int tiles_x, 
 // H1 for the tiles the warp kernel handed over (more foreground than its
 // compact lists hold): one 128-thread block per tile.
 __global__ void __launch_bounds__(H_THREADS)
-hyst_dense_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
-                  uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
+hyst_dense_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t* __restrict__ final_out, HystBufs b,
+                  WsHeader* hdr) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
     const unsigned n = hdr->dense_count;
     for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
         const long long tile = b.dense[e];
-        hyst_block_tile(labels, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
     }
 }
 
@@ -505,9 +525,8 @@ constexpr int WCAP = EF_H1_WCAP;
 constexpr int WT_WARPS = EF_H1_WARPS;  // tiles per block (small: a block holds its slot until its slowest tile ends)
 
 struct WarpTile {
-    unsigned long long fgrow[HT];
-    unsigned long long strow[HT];
-    unsigned long long finrow[HT];
+    unsigned long long fgrow[HT];  // weak pixels
+    unsigned long long strow[HT];  // weak pixels next to a strong pixel (seeds)
     unsigned short rowbase[HT + 1];
     unsigned short par[WCAP];
     unsigned short info[WCAP];  // as TileCCL::info, per compact index
@@ -524,14 +543,6 @@ __device__ __forceinline__ int wfind(const unsigned short* par, int i) {  // rea
         if (p == i) return i;
         i = p;
     }
-}
-
-// 16 bits -> 16 bytes (0/1)
-__device__ __forceinline__ uint4 expand16(uint32_t bits) {
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = (((bits >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u;
-    return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 // k-th (0-based) set bit of m
@@ -569,10 +580,9 @@ __device__ __forceinline__ int row_of(const WarpTile& s, int e) {
 // pixel instead of its label bytes and stores only weak pixels that join an
 // edge.  Otherwise the label bytes are read and the whole final tile written.
 // Grid: (ceil(tiles per frame / WT_WARPS), frames); one warp per tile.
-template <bool BITS>
 __global__ void __launch_bounds__(32 * WT_WARPS)
-hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
-                       uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr, FgBits B) {
+hyst_local_warp_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t* __restrict__ final_out, HystBufs b,
+                       WsHeader* hdr) {
     __shared__ WarpTile tiles[WT_WARPS];
     pdl_wait();
     pdl_trigger();
@@ -586,68 +596,36 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
     const long long tile = (long long)blockIdx.y * tpf + t;
     const int stripe = t % PL_STRIPES;  // == tile % PL_STRIPES only up to the frame offset: any stripe works
     const size_t frame_off = (size_t)g.f * H * W;
-    const int q = lane & 3, rsub = lane >> 2;  // label path: 4 lanes per row, 16 bytes each
-    if (BITS) {
-        // rows 2*lane, 2*lane+1 of word column tx
-        const unsigned long long w0 =
-            (unsigned long long)g.f * B.frame_words + (unsigned long long)(g.y0 + 2 * lane) * B.words + g.txi;
-        const bool r0 = 2 * lane < g.vh, r1 = 2 * lane + 1 < g.vh;
-        s.fgrow[2 * lane] = r0 ? __ldg(B.fg + w0) : 0ull;
-        s.strow[2 * lane] = r0 ? __ldg(B.st + w0) : 0ull;
-        s.fgrow[2 * lane + 1] = r1 ? __ldg(B.fg + w0 + B.words) : 0ull;
-        s.strow[2 * lane + 1] = r1 ? __ldg(B.st + w0 + B.words) : 0ull;
-    } else {
-        // all eight 16-byte loads are issued before any is consumed (one DRAM
-        // round trip per tile, not eight)
-        const bool full_in = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(labels) & 15) == 0);
-        uint4 v[HT / 8];
-        const uint8_t* src0 = labels + frame_off + (size_t)(g.y0 + rsub) * W + g.x0 + 16 * q;
-#pragma unroll
-        for (int it = 0; it < HT / 8; ++it) {
-            const int r = it * 8 + rsub;
-            v[it] = make_uint4(0u, 0u, 0u, 0u);
-            if (r < g.vh) {
-                const uint8_t* src = src0 + (size_t)(it * 8) * W;
-                if (full_in) {
-                    v[it] = __ldg(reinterpret_cast<const uint4*>(src));
-                } else {
-                    uint32_t w4[4] = {0u, 0u, 0u, 0u};
-                    for (int k = 0; k < 16 && 16 * q + k < g.vw; ++k) w4[k >> 2] |= (uint32_t)src[k] << (8 * (k & 3));
-                    v[it] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                }
-            }
+    // rows 2*lane, 2*lane+1: weak pixels (f) and strong pixels (t)
+    const int ya = g.y0 + 2 * lane;
+    const unsigned long long t0 = plane_word(B.st, B, g.f, ya, H, g.txi);
+    const unsigned long long t1 = plane_word(B.st, B, g.f, ya + 1, H, g.txi);
+    const unsigned long long f0 = plane_word(B.fg, B, g.f, ya, H, g.txi) & ~t0;
+    const unsigned long long f1 = plane_word(B.fg, B, g.f, ya + 1, H, g.txi) & ~t1;
+    const bool any_weak = __any_sync(0xffffffffu, (f0 | f1) != 0ull);
+    if (!any_weak) {  // final as it stands (the final map holds its strong pixels); nothing to export
+        if (lane == 0) {
+            b.border[tile] = 0;
+            b.pending[tile] = 0;
         }
-#pragma unroll
-        for (int it = 0; it < HT / 8; ++it) {
-            const int r = it * 8 + rsub;
-            const uint32_t w4[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
-            uint32_t f16 = 0, s16 = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t f, tt;
-                pack4(w4[j], f, tt);
-                f16 |= f << (4 * j);
-                s16 |= tt << (4 * j);
-            }
-            // gather the row's four quarters (lanes 4*rsub .. 4*rsub+3)
-            unsigned long long fr = (unsigned long long)f16 << (16 * q);
-            unsigned long long sr = (unsigned long long)s16 << (16 * q);
-            fr |= __shfl_xor_sync(0xffffffffu, fr, 1);
-            sr |= __shfl_xor_sync(0xffffffffu, sr, 1);
-            fr |= __shfl_xor_sync(0xffffffffu, fr, 2);
-            sr |= __shfl_xor_sync(0xffffffffu, sr, 2);
-            if (q == 0) {
-                s.fgrow[r] = fr;
-                s.strow[r] = sr;
-            }
-        }
+        return;
     }
+    // seeds: weak pixels 8-adjacent to a strong pixel -- the strong rows above
+    // and below from the neighbouring lanes (the tiles above / below for lanes
+    // 0 and 31), the neighbouring words' edge bits only where a weak pixel sits
+    // at column 0 or 63
+    unsigned long long up = __shfl_up_sync(0xffffffffu, t1, 1), dn = __shfl_down_sync(0xffffffffu, t0, 1);
+    if (lane == 0) up = plane_word(B.st, B, g.f, g.y0 - 1, H, g.txi);
+    if (lane == 31) dn = plane_word(B.st, B, g.f, g.y0 + HT, H, g.txi);
+    const unsigned long long v0 = up | t0 | t1, v1 = t0 | t1 | dn;
+    const unsigned long long s0 = f0 ? f0 & (v0 | (v0 << 1) | (v0 >> 1) | side_strong(B, g.f, ya, H, g.txi, f0)) : 0ull;
+    const unsigned long long s1 =
+        f1 ? f1 & (v1 | (v1 << 1) | (v1 >> 1) | side_strong(B, g.f, ya + 1, H, g.txi, f1)) : 0ull;
+    s.fgrow[2 * lane] = f0;
+    s.fgrow[2 * lane + 1] = f1;
+    s.strow[2 * lane] = s0;
+    s.strow[2 * lane + 1] = s1;
     __syncwarp();
-    // ---- each lane owns rows 2*lane, 2*lane+1 for the prefix counts
-    const unsigned long long f0 = s.fgrow[2 * lane], f1 = s.fgrow[2 * lane + 1];
-    const unsigned long long s0 = s.strow[2 * lane], s1 = s.strow[2 * lane + 1];
-    const bool any_fg = __any_sync(0xffffffffu, (f0 | f1) != 0ull);
-    const bool any_weak = __any_sync(0xffffffffu, ((f0 & ~s0) | (f1 & ~s1)) != 0ull);
     const int c0 = __popcll(f0), c1 = __popcll(f1);
     int incl = c0 + c1;
 #pragma unroll
@@ -656,22 +634,19 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         if (lane >= d) incl += v;
     }
     const int n = __shfl_sync(0xffffffffu, incl, 31);
-    if (any_weak && n > WCAP) {  // dense tile: the block kernel takes it (reads the labels)
+    if (n > WCAP) {  // dense tile: the block kernel takes it
         if (lane == 0) b.dense[atomicAdd(&hdr->dense_count, 1u)] = (int)tile;
         return;
     }
-    const int kind = any_fg ? (any_weak ? 2 : 1) : 0;  // empty, strong only, general
     bool tile_pending = false;
-    if (kind) {
+    {
         const int base0 = incl - c0 - c1;
         s.rowbase[2 * lane] = (unsigned short)base0;
         s.rowbase[2 * lane + 1] = (unsigned short)(base0 + c0);
         if (lane == 31) s.rowbase[HT] = (unsigned short)n;
-        s.finrow[2 * lane] = 0ull;
-        s.finrow[2 * lane + 1] = 0ull;
         __syncwarp();
     }
-    if (kind == 2) {
+    {
         // compact list + union-find init, lane-balanced: index e -> (row, column)
         // by the prefix counts; runs are pre-linked to their start
         for (int e = lane; e < n; e += 32) {
@@ -680,6 +655,7 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
             const int x = select64(fr, e - s.rowbase[r]);
             const unsigned long long below = ~fr & ((1ull << x) - 1ull);
             const int start = below ? 64 - __clzll((long long)below) : 0;
+            EF_DCHECK(e < WCAP && r >= 0 && r < HT && x >= 0 && x < HT && ((fr >> x) & 1ull) && start <= x);
             s.list[e] = (unsigned short)(r * HT + x);
             s.par[e] = (unsigned short)(e - (x - start));
             s.info[e] = 0xffffu;
@@ -697,6 +673,8 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
             const bool in_run = x > 0 && ((s.fgrow[r] >> (x - 1)) & 1ull);
             const bool nx = (up >> x) & 1ull;
             const bool nr = x < HT - 1 && ((up >> (x + 1)) & 1ull);
+            EF_DCHECK(!nx || cidx(s, r - 1, x) < n);
+            EF_DCHECK(!nr || cidx(s, r - 1, x + 1) < n);
             if (in_run) {
                 if (nr && !nx) sunite(s.par, e, cidx(s, r - 1, x + 1));
             } else if (nx) {
@@ -708,7 +686,7 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
         __syncwarp();
         // roots (read-only finds, so par[e] = root can be written at once) and
-        // per-component strong flag / smallest perimeter slot
+        // per-component strong flag (a seed: next to a strong pixel) / smallest perimeter slot
         for (int e = lane; e < n; e += 32) {
             const int pix = s.list[e];
             const int r = pix >> 6, x = pix & (HT - 1);
@@ -719,7 +697,8 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
             if (p != NO_POS) info_min_slot(&s.info[root], (unsigned)p);
         }
         __syncwarp();
-        // final pixels; undecided border components -> pending list
+        // final pixels (weak pixels of strong components); undecided border
+        // components -> pending list
         for (int e0 = 0; e0 < n; e0 += 32) {
             const int e = e0 + lane;
             bool pend = false;
@@ -729,9 +708,8 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
                 pix = s.list[e];
                 v = s.info[s.par[e]];
                 if (info_strong(v)) {
-                    if (!BITS) atomicOr(&s.finrow[pix >> 6], 1ull << (pix & (HT - 1)));
-                    else if (!((s.strow[pix >> 6] >> (pix & (HT - 1))) & 1ull))  // weak pixel joins an edge
-                        final_out[frame_off + (size_t)(g.y0 + (pix >> 6)) * W + g.x0 + (pix & (HT - 1))] = 1;
+                    EF_DCHECK((pix >> 6) < g.vh && (pix & (HT - 1)) < g.vw);
+                    final_out[frame_off + (size_t)(g.y0 + (pix >> 6)) * W + g.x0 + (pix & (HT - 1))] = 1;
                 } else {
                     pend = info_slot(v) != NO_SLOT;
                 }
@@ -754,28 +732,9 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         }
         __syncwarp();
     }
-    if (!BITS) {
-        // ---- whole final tile (4 lanes per row, 16 bytes each).  (BITS: the
-        // classifier wrote final = strong for every pixel; only the weak
-        // pixels joining an edge are stored above.)
-        const bool full_out = g.vw == HT && ((W & 15) == 0) && ((reinterpret_cast<uintptr_t>(final_out) & 15) == 0);
-#pragma unroll 2
-        for (int it = 0; it < HT / 8; ++it) {
-            const int r = it * 8 + rsub;
-            if (r >= g.vh) continue;
-            const unsigned long long fr = kind == 2 ? s.finrow[r] : (kind == 1 ? s.fgrow[r] : 0ull);
-            const uint32_t bits = (uint32_t)(fr >> (16 * q)) & 0xffffu;
-            uint8_t* dst = final_out + frame_off + (size_t)(g.y0 + r) * W + g.x0 + 16 * q;
-            if (full_out) {
-                *reinterpret_cast<uint4*>(dst) = expand16(bits);
-            } else {
-                for (int k = 0; k < 16 && 16 * q + k < g.vw; ++k) dst[k] = (uint8_t)((bits >> k) & 1u);
-            }
-        }
-    }
-    // ---- perimeter slots (lane handles slots lane + 32 j): node id of the
+    // ---- perimeter slots (lane handles slots lane + 32 j): node id of the weak
     // component at each slot; a component's own (smallest) slot makes it a node.
-    // A tile without foreground on its perimeter writes nothing here: its
+    // A tile without weak pixels on its perimeter writes nothing here: its
     // border flag tells every reader of perim[] (H2, H3's fallback scan, the
     // band-edge export) to skip it.
     const unsigned long long vmask = g.vw == HT ? ~0ull : ((1ull << g.vw) - 1ull);
@@ -800,25 +759,16 @@ hyst_local_warp_kernel(const uint8_t* __restrict__ labels, int H, int W, int til
         const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
         int node = -1;
         bool mine = false;
-        if (kind && valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
-            if (kind == 1) {
-                const int sl = perim_slot(y, x, g.vh, g.vw);
-                node = (int)(tile * HP) + sl;
-                if (sl == p) {
-                    mine = true;
-                    b.gpar[node] = node;
-                    b.gstrong[node] = 1;
-                }
-            } else {
-                const unsigned v = s.info[s.par[cidx(s, y, x)]];
-                node = (int)(tile * HP) + (int)info_slot(v);
-                if (info_slot(v) == (unsigned)p) {
-                    mine = true;
-                    b.gpar[node] = node;
-                    b.gstrong[node] = info_strong(v) ? 1 : 0;
-                }
+        if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
+            const unsigned v = s.info[s.par[cidx(s, y, x)]];
+            node = (int)(tile * HP) + (int)info_slot(v);
+            if (info_slot(v) == (unsigned)p) {
+                mine = true;
+                b.gpar[node] = node;
+                b.gstrong[node] = info_strong(v) ? 1 : 0;
             }
         }
+        EF_DCHECK(p >= 0 && p < HP && (node < 0 || (node >= tile * HP && node < (tile + 1) * HP)));
         b.perim[tile * HP + p] = node;
         nodes[j] = node;
         own[j] = __ballot_sync(0xffffffffu, mine);
@@ -969,7 +919,7 @@ __global__ void hyst_resolve_kernel(long long nslots, HystBufs b, WsHeader* hdr)
 }
 
 struct TileCCL;
-__device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+__device__ void hyst_final_tile(const FgBits& B, int H, int W, int tiles_x, int tiles_y,
                                 uint8_t* __restrict__ final_out, const HystBufs& b, long long tile, TileCCL& s);
 
 // H4: pixels of undecided border components read their root's strong flag,
@@ -980,8 +930,8 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
 // Grid (x, PL_STRIPES), H_THREADS threads: list mode reads stripe blockIdx.y;
 // overflow mode walks the tiles over the flattened grid.
 __global__ void __launch_bounds__(H_THREADS)
-hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, int frames,
-                  uint8_t* __restrict__ final_out, HystBufs b, const WsHeader* __restrict__ hdr) {
+hyst_final_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, int frames, uint8_t* __restrict__ final_out,
+                  HystBufs b, const WsHeader* __restrict__ hdr) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
@@ -996,11 +946,11 @@ hyst_final_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x,
     const long long ntiles = (long long)tiles_x * tiles_y * frames;
     const long long nblocks = (long long)gridDim.x * gridDim.y;
     for (long long tile = (long long)blockIdx.y * gridDim.x + blockIdx.x; tile < ntiles; tile += nblocks) {
-        if (b.pending[tile]) hyst_final_tile(labels, H, W, tiles_x, tiles_y, final_out, b, tile, s);
+        if (b.pending[tile]) hyst_final_tile(B, H, W, tiles_x, tiles_y, final_out, b, tile, s);
     }
 }
 
-__device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y,
+__device__ void hyst_final_tile(const FgBits& B, int H, int W, int tiles_x, int tiles_y,
                                 uint8_t* __restrict__ final_out, const HystBufs& b, long long tile, TileCCL& s) {
     const int txi = (int)(tile % tiles_x);
     const long long rest = tile / tiles_x;
@@ -1008,7 +958,7 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
     if (threadIdx.x == 0) s.flags = 0;
     __syncthreads();
     uint32_t fg, st;
-    tile_load(labels, H, W, g, s, fg, st);
+    tile_load(B, H, g, s, fg, st);
     __syncthreads();
     tile_ccl(g, s, fg, st, !(s.flags & 4));
     const int tid = threadIdx.x;
@@ -1028,9 +978,12 @@ __device__ void hyst_final_tile(const uint8_t* __restrict__ labels, int H, int W
 
 // Band edge export: component root id and strong flag for the top and bottom
 // rows of a band (the frame of `rows` rows).
+// Strong pixels are not union-find nodes: a strong pixel on an edge row is
+// exported as a strong singleton (id 2^39 + entry, unique inside the band), so
+// the cross-band merge makes the weak components next to it strong.
 __global__ void band_edges_kernel(int rows, int W, int tiles_x, int tiles_y, const int* __restrict__ perim,
                                   const uint8_t* __restrict__ border, const int* __restrict__ gpar,
-                                  const uint8_t* __restrict__ gstrong, int64_t* ids, uint8_t* strong) {
+                                  const uint8_t* __restrict__ gstrong, FgBits B, int64_t* ids, uint8_t* strong) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2 * W) return;
     bool bottom = t >= W;
@@ -1038,7 +991,13 @@ __global__ void band_edges_kernel(int rows, int W, int tiles_x, int tiles_y, con
     long long tile = (long long)(bottom ? tiles_y - 1 : 0) * tiles_x + x / HT;
     int slot = (bottom ? 64 : 0) + x % HT;
     int node = border[tile] ? perim[tile * HP + slot] : -1;
-    if (node < 0) { ids[t] = -1; strong[t] = 0; return; }
+    if (node < 0) {
+        const int y = bottom ? rows - 1 : 0;
+        const bool st = (__ldg(B.st + (unsigned long long)y * B.words + (x >> 6)) >> (x & 63)) & 1ull;
+        ids[t] = st ? (int64_t)((1ll << 39) + t) : -1;
+        strong[t] = st ? 1 : 0;
+        return;
+    }
     int r = gfind_ro(gpar, node);
     ids[t] = r;
     strong[t] = gstrong[r];
@@ -1077,13 +1036,69 @@ HystLayout hyst_layout(int64_t batch, int H, int W) {
 // launches with few tiles, where one warp per tile leaves the SMs idle while
 // each warp walks a large tile's union-find alone.
 __global__ void __launch_bounds__(H_THREADS)
-hyst_all_block_kernel(const uint8_t* __restrict__ labels, int H, int W, int tiles_x, int tiles_y, long long ntiles,
+hyst_all_block_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, long long ntiles,
                       uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        hyst_block_tile(labels, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+}
+
+// Label bytes (0/1/2) -> the two foreground bit planes, one thread per 64-bit
+// word (the hysteresis input when no classifier filled the planes: standalone
+// tracing, the exact float64 path, the generic classifier).
+__global__ void hyst_pack_kernel(const uint8_t* __restrict__ labels, long long rows, int W, int words,
+                                 unsigned long long* __restrict__ fg, unsigned long long* __restrict__ st) {
+    pdl_wait();
+    pdl_trigger();
+    const long long n = rows * words;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / words;
+        const int j = (int)(i - row * words);
+        const uint8_t* p = labels + row * W + 64 * j;
+        const int cnt = min(64, W - 64 * j);
+        unsigned long long f = 0, s2 = 0;
+        if (cnt == 64 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t a, c;
+                    pack4(w4[k], a, c);
+                    f |= (unsigned long long)a << (16 * q + 4 * k);
+                    s2 |= (unsigned long long)c << (16 * q + 4 * k);
+                }
+            }
+        } else {
+            for (int k = 0; k < cnt; ++k) {
+                const uint32_t v = p[k];
+                f |= (unsigned long long)(v != 0u) << k;
+                s2 |= (unsigned long long)(v >= 2u) << k;
+            }
+        }
+        fg[i] = f;
+        st[i] = s2;
+    }
+}
+
+// final = strong for every pixel (the classifier writes this itself in the
+// fused path; the hysteresis then adds the weak pixels that join an edge)
+__global__ void strong_final_kernel(const uint8_t* __restrict__ labels, long long n, uint8_t* __restrict__ fin) {
+    pdl_wait();
+    pdl_trigger();
+    const bool vec = ((reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(fin)) & 15) == 0;
+    const long long nv = vec ? n / 16 : 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(labels) + i);
+        reinterpret_cast<uint4*>(fin)[i] = make_uint4((v.x >> 1) & 0x01010101u, (v.y >> 1) & 0x01010101u,
+                                                      (v.z >> 1) & 0x01010101u, (v.w >> 1) & 0x01010101u);
+    }
+    for (long long i = nv * 16 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        fin[i] = labels[i] >= 2 ? 1 : 0;
 }
 
 // tiles per SM at or below which H1 runs one block per tile (ef_set_block_tile_threshold)
@@ -1093,17 +1108,14 @@ static std::atomic<int> g_block_tiles_per_sm{getenv("EF_H1_BLOCK_TILES_PER_SM") 
 
 void set_block_tile_threshold(int tiles_per_sm) { g_block_tiles_per_sm.store(tiles_per_sm); }
 
-cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
-                              cudaStream_t st) {
+cudaError_t launch_hyst_local(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, const HystBufs& b,
+                              WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
-    // shared memory bound (5 KB per warp tile, 20 KB per dense tile): full carveout
+    // shared memory bound (~5 KB per warp tile, ~21 KB per dense tile): full carveout
     static std::atomic<uint64_t> configured{0};
     cudaError_t e = once_per_device(configured, [] {
         const int c = (int)cudaSharedmemCarveoutMaxShared;
-        cudaError_t r = cudaFuncSetAttribute(hyst_local_warp_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-        if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(hyst_local_warp_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+        cudaError_t r = cudaFuncSetAttribute(hyst_local_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
         if (r == cudaSuccess) r = cudaFuncSetAttribute(hyst_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
         if (r == cudaSuccess)
             r = cudaFuncSetAttribute(hyst_all_block_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
@@ -1115,18 +1127,15 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
     if (allblock) {
         // few tiles: a block per tile (the dense-tile list stays empty)
         e = launch_pdl(hyst_all_block_kernel, dim3((unsigned)std::min<int64_t>(L.tiles, 16ll * sm_count)),
-                           dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x, L.tiles_y, (long long)L.tiles, final_out,
-                           b, hdr);
-    } else if (bits)
-        e = launch_pdl(hyst_local_warp_kernel<true>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
-                       L.tiles_y, final_out, b, hdr, *bits);
-    else
-        e = launch_pdl(hyst_local_warp_kernel<false>, wgrid, dim3(32 * WT_WARPS), 0, st, labels, H, W, L.tiles_x,
-                       L.tiles_y, final_out, b, hdr, FgBits{});
+                       dim3(H_THREADS), 0, st, B, H, W, L.tiles_x, L.tiles_y, (long long)L.tiles, final_out, b, hdr);
+    } else {
+        e = launch_pdl(hyst_local_warp_kernel, wgrid, dim3(32 * WT_WARPS), 0, st, B, H, W, L.tiles_x, L.tiles_y,
+                       final_out, b, hdr);
+    }
     if (e != cudaSuccess) return e;
     if (!allblock) {  // the block kernel took every tile: the dense list is empty
-        e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, labels, H, W, L.tiles_x,
-                       L.tiles_y, final_out, b, hdr);
+        e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, B, H, W, L.tiles_x, L.tiles_y,
+                       final_out, b, hdr);
         if (e != cudaSuccess) return e;
     }
     const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);
@@ -1136,18 +1145,31 @@ cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W
                       (long long)L.slots, b, hdr);
 }
 
-cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st) {
+cudaError_t launch_hyst_final(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, const HystBufs& b,
+                              const WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
     return launch_pdl(hyst_final_kernel, dim3(stripe_blocks(L.tiles, sm_count), PL_STRIPES), dim3(H_THREADS), 0,
-                      st, labels, H, W, L.tiles_x, L.tiles_y, (int)batch, final_out, b, hdr);
+                      st, B, H, W, L.tiles_x, L.tiles_y, (int)batch, final_out, b, hdr);
 }
 
-cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
+cudaError_t launch_hyst_pack(const uint8_t* labels, int64_t batch, int H, int W, const FgBits& B, int sm_count,
+                             cudaStream_t st) {
+    const long long n = batch * (long long)H * B.words;
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 8ll * sm_count));
+    return launch_pdl(hyst_pack_kernel, dim3(grid), dim3(256), 0, st, labels, batch * (long long)H, W, B.words, B.fg,
+                      B.st);
+}
+
+cudaError_t launch_strong_final(const uint8_t* labels, long long n, uint8_t* fin, int sm_count, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((n / 16 + 255) / 256, 8ll * sm_count));
+    return launch_pdl(strong_final_kernel, dim3(grid), dim3(256), 0, st, labels, n, fin);
+}
+
+cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, const FgBits& B, int64_t* ids, uint8_t* strong,
                               cudaStream_t st) {
     HystLayout L = hyst_layout(1, rows, W);
     band_edges_kernel<<<(2 * W + 255) / 256, 256, 0, st>>>(rows, W, L.tiles_x, L.tiles_y, b.perim, b.border, b.gpar,
-                                                           b.gstrong, ids, strong);
+                                                           b.gstrong, B, ids, strong);
     return cudaGetLastError();
 }
 

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ef_common.cuh"  // EF_DCHECK
+
 namespace ef {
 
 struct ExactParams;
@@ -89,6 +91,7 @@ struct FgBits {
 __device__ __forceinline__ void fg_bits_or(const FgBits& B, unsigned long long f, int yo, int x, uint32_t fgn,
                                            uint32_t stn) {
     const unsigned long long w = f * B.frame_words + (unsigned long long)yo * B.words + (unsigned)(x >> 6);
+    EF_DCHECK(B.st - B.fg >= 0 && w < (unsigned long long)(B.st - B.fg) && (x & 3) == 0 && (unsigned)(x >> 6) < (unsigned)B.words);
     // global-space reductions (no return value): stated explicitly -- through
     // pointers the compiler could not prove global (an out-of-line classifier)
     // these compiled to generic atomics with shared-space checks (K1 +3%)
@@ -131,14 +134,18 @@ cudaError_t launch_fix(const uint8_t* src, int64_t batch, const FrameGeom& g, co
                        int sm_count, cudaStream_t st);
 
 HystLayout hyst_layout(int64_t batch, int H, int W);
-// bits: the classifier's foreground bit planes for these labels (final_out
-// zeroed beforehand), or nullptr to read the label bytes
-cudaError_t launch_hyst_local(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, WsHeader* hdr, const FgBits* bits, int sm_count,
-                              cudaStream_t st);
-cudaError_t launch_hyst_final(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* final_out,
-                              const HystBufs& b, const WsHeader* hdr, int sm_count, cudaStream_t st);
-cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, int64_t* ids, uint8_t* strong,
+// Hysteresis over the foreground bit planes B (label != 0, label == 2), with
+// final_out already holding final = strong: H1 (+ dense tiles), H2, H3.
+cudaError_t launch_hyst_local(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, const HystBufs& b,
+                              WsHeader* hdr, int sm_count, cudaStream_t st);
+// H4: pending weak pixels read their root's flag
+cudaError_t launch_hyst_final(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, const HystBufs& b,
+                              const WsHeader* hdr, int sm_count, cudaStream_t st);
+// label bytes -> bit planes; final = strong (callers without the fused classifier)
+cudaError_t launch_hyst_pack(const uint8_t* labels, int64_t batch, int H, int W, const FgBits& B, int sm_count,
+                             cudaStream_t st);
+cudaError_t launch_strong_final(const uint8_t* labels, long long n, uint8_t* fin, int sm_count, cudaStream_t st);
+cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, const FgBits& B, int64_t* ids, uint8_t* strong,
                               cudaStream_t st);
 cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,
                               cudaStream_t st);
