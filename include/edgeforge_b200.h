@@ -65,6 +65,12 @@ typedef struct ef_stats {
  * warp per tile.  The result is identical either way. */
 int ef_set_block_tile_threshold(int32_t tiles_per_sm);
 
+/* Hysteresis tuning: 1 (default) = the tile pass first grows the weak pixels
+ * reached from the tile's seeds (final at once) and runs its union-find only
+ * over the unreached components touching the tile perimeter; 0 = union-find
+ * over every weak pixel.  The result is identical either way. */
+int ef_set_tile_reach(int32_t on);
+
 /* Which capacity fallbacks the last call on this workspace took (synchronises
  * `stream`): h_out[0] fix list overflowed (FX scanned every label), [1] a
  * pending-list stripe overflowed (H4 re-ran the pending tiles), [2] tiles H1's

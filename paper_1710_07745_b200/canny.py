@@ -307,6 +307,11 @@ def set_block_tile_threshold(tiles_per_sm: int) -> None:
     _lib.check(_lib.load().ef_set_block_tile_threshold(int(tiles_per_sm)), "ef_set_block_tile_threshold")
 
 
+def set_tile_reach(on: bool) -> None:
+    """Hysteresis tuning: tile-local reach before the tile union-find (default on)."""
+    _lib.check(_lib.load().ef_set_tile_reach(1 if on else 0), "ef_set_tile_reach")
+
+
 def read_paths(ws, stream=None) -> dict:
     """Capacity fallbacks the last call on `ws` took (ef_read_paths)."""
     out = (ctypes.c_uint32 * 4)()

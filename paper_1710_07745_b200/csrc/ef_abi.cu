@@ -419,6 +419,12 @@ int ef_set_block_tile_threshold(int32_t tiles_per_sm) {
     return EF_OK;
 }
 
+int ef_set_tile_reach(int32_t on) {
+    if (on != 0 && on != 1) return fail(EF_EINVAL, "on must be 0 or 1");
+    set_tile_reach(on);
+    return EF_OK;
+}
+
 int ef_read_paths(const void* d_workspace, size_t workspace_bytes, void* stream, uint32_t* h_out) {
     if (!d_workspace || workspace_bytes < sizeof(WsHeader) || !h_out) return fail(EF_EINVAL, "bad arguments");
     EF_CHECK(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");

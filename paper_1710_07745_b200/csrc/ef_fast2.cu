@@ -57,6 +57,9 @@ constexpr int V2_COLS = 128;
 #ifndef EF_K1_POOL
 #define EF_K1_POOL 1  // phase 3 pools the four warps' candidates (0: each warp classifies its own rows)
 #endif
+#ifndef EF_K1_HODD
+#define EF_K1_HODD 1  // odd horizontal taps as one FFMA2 over two scalar sums (0: four scalar ops)
+#endif
 #ifndef EF_K1_MINB
 #define EF_K1_MINB 6  // CTAs per SM the register budget is sized for (shared memory allows 6 at TH = 32)
 #endif
@@ -190,6 +193,10 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
             if ((o & 1) == 0) {
                 b01 = fma2(wf2[o], add2(f2(e[8 - o], e[9 - o]), f2(e[8 + o], e[9 + o])), b01);
                 b23 = fma2(wf2[o], add2(f2(e[10 - o], e[11 - o]), f2(e[10 + o], e[11 + o])), b23);
+            } else if (EF_K1_HODD) {
+                // odd taps: the two sums land in a register pair, one FFMA2
+                b01 = fma2(wf2[o], f2(e[8 - o] + e[8 + o], e[9 - o] + e[9 + o]), b01);
+                b23 = fma2(wf2[o], f2(e[10 - o] + e[10 + o], e[11 - o] + e[11 + o]), b23);
             } else {
                 b01.x = fmaf(wf2[o].x, e[8 - o] + e[8 + o], b01.x);
                 b01.y = fmaf(wf2[o].x, e[9 - o] + e[9 + o], b01.y);
@@ -368,6 +375,9 @@ struct V3Smem {
     unsigned cmask[V2_TH];                          // candidate 4-pixel groups per output row (bit = lane)
     unsigned long long mbar;
     FgBits bits;
+#ifdef EF_K1_SMEM_PAD
+    unsigned char pad[EF_K1_SMEM_PAD];  // occupancy experiments only
+#endif
 };
 static_assert(offsetof(V3Smem, in) % 128 == 0 && offsetof(V3Smem, b) % 16 == 0, "TMA / float4 alignment");
 static_assert(EF_K1_MINB * (sizeof(V3Smem) + 1024) <= 233472, "CTAs per SM the register budget assumes fit in shared memory");

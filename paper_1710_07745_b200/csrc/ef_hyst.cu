@@ -242,17 +242,31 @@ __device__ __forceinline__ void weak_row(const FgBits& B, int f, int Y, int rows
 // words and flags.  Also initialises union-find state for its weak pixels
 // (runs inside the 32-pixel segment pre-linked to their start) and appends
 // them to the warp's pixel list.  The caller's barrier makes everything visible.
+__device__ __forceinline__ void tile_init(TileCCL& s, unsigned long long wk, unsigned long long seed,
+                                          unsigned long long strong, bool publish, uint32_t& fg, uint32_t& st);
+
 __device__ __forceinline__ void tile_load(const FgBits& B, int rows, const TileGeo& g, TileCCL& s, uint32_t& fg,
                                           uint32_t& st) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int row = tid >> 1, seg = (tid & 1) * 32;
+    const int row = threadIdx.x >> 1;
     unsigned long long wk = 0, seed = 0, strong = 0;
     if (row < g.vh) weak_row(B, g.f, g.y0 + row, rows, g.txi, wk, seed, strong);
+    tile_init(s, wk, seed, strong, true, fg, st);
+}
+
+// The second half of tile_load: this thread's 32-pixel segment of the row
+// words (published to the tile's rows unless they are there already) -> par /
+// info / list initialisation and the tile flags.
+__device__ __forceinline__ void tile_init(TileCCL& s, unsigned long long wk, unsigned long long seed,
+                                          unsigned long long strong, bool publish, uint32_t& fg, uint32_t& st) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = tid >> 1, seg = (tid & 1) * 32;
     fg = (uint32_t)(wk >> seg);
     st = (uint32_t)(seed >> seg);
-    reinterpret_cast<uint32_t*>(&s.fgrow[row])[tid & 1] = fg;
-    reinterpret_cast<uint32_t*>(&s.strow[row])[tid & 1] = st;
-    reinterpret_cast<uint32_t*>(&s.st0[row])[tid & 1] = (uint32_t)(strong >> seg);
+    if (publish) {
+        reinterpret_cast<uint32_t*>(&s.fgrow[row])[tid & 1] = fg;
+        reinterpret_cast<uint32_t*>(&s.strow[row])[tid & 1] = st;
+        reinterpret_cast<uint32_t*>(&s.st0[row])[tid & 1] = (uint32_t)(strong >> seg);
+    }
     // warp-exclusive prefix of the foreground counts -> list positions
     const int cnt = __popc(fg);
     int off = cnt;
@@ -387,6 +401,92 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Tile-local reach (before the union-find).  A weak component of the tile
+// either holds a seed -- then every pixel of it is final -- or it does not;
+// the latter decide nothing inside the tile, and only those touching the tile
+// perimeter can still be joined to a strong pixel through a neighbour tile.
+// Both sets come from a bit-parallel fixpoint over the warp's row words (lane
+// = rows 2*lane, 2*lane+1; x = x | dilate8(x) & W, tile-local): typically 1-3
+// rounds on Canny maps (C3: 95% of the weak pixels are not reached, 12% touch
+// the perimeter).  The union-find then runs only over the perimeter-touching
+// unreached components plus the reached pixels on the perimeter (strong
+// singletons for the seams), so a perimeter component keeps the node id the
+// full CCL gives it (the smallest perimeter slot of the same weak component:
+// H4's overflow path re-runs the full CCL and must agree).  More than
+// EF_H1_REACH_ITERS rounds (long snakes, mazes): the full sets are kept.
+#ifndef EF_H1_REACH
+#define EF_H1_REACH 1
+#endif
+#ifndef EF_H1_REACH_ITERS
+#define EF_H1_REACH_ITERS 48
+#endif
+
+// rows 2*lane, 2*lane+1 of the tile: weak pixels and their seeds (weak pixels
+// 8-adjacent to a strong pixel: the strong rows above and below from the
+// neighbouring lanes -- the tiles above / below for lanes 0 and 31 -- and the
+// neighbouring words' edge bits only where a weak pixel sits at column 0 or 63)
+__device__ __forceinline__ void warp_rows(const FgBits& B, const TileGeo& g, int lane, int H, unsigned long long& f0,
+                                          unsigned long long& f1, unsigned long long& s0, unsigned long long& s1) {
+    const int ya = g.y0 + 2 * lane;
+    const unsigned long long t0 = plane_word(B.st, B, g.f, ya, H, g.txi);
+    const unsigned long long t1 = plane_word(B.st, B, g.f, ya + 1, H, g.txi);
+    f0 = plane_word(B.fg, B, g.f, ya, H, g.txi) & ~t0;
+    f1 = plane_word(B.fg, B, g.f, ya + 1, H, g.txi) & ~t1;
+    unsigned long long up = __shfl_up_sync(0xffffffffu, t1, 1), dn = __shfl_down_sync(0xffffffffu, t0, 1);
+    if (lane == 0) up = plane_word(B.st, B, g.f, g.y0 - 1, H, g.txi);
+    if (lane == 31) dn = plane_word(B.st, B, g.f, g.y0 + HT, H, g.txi);
+    const unsigned long long v0 = up | t0 | t1, v1 = t0 | t1 | dn;
+    s0 = f0 ? f0 & (v0 | (v0 << 1) | (v0 >> 1) | side_strong(B, g.f, ya, H, g.txi, f0)) : 0ull;
+    s1 = f1 ? f1 & (v1 | (v1 << 1) | (v1 >> 1) | side_strong(B, g.f, ya + 1, H, g.txi, f1)) : 0ull;
+}
+
+// x grows inside w by 8-adjacency (tile-local) until it stops changing;
+// false if it still changed after EF_H1_REACH_ITERS rounds
+__device__ __forceinline__ bool warp_grow(unsigned long long w0, unsigned long long w1, unsigned long long& x0,
+                                          unsigned long long& x1, int lane) {
+    for (int it = 0; it < EF_H1_REACH_ITERS; ++it) {
+        const unsigned long long d0 = x0 | (x0 << 1) | (x0 >> 1), d1 = x1 | (x1 << 1) | (x1 >> 1);
+        unsigned long long up = __shfl_up_sync(0xffffffffu, d1, 1), dn = __shfl_down_sync(0xffffffffu, d0, 1);
+        if (lane == 0) up = 0;
+        if (lane == 31) dn = 0;
+        const unsigned long long n0 = w0 & (up | d0 | d1), n1 = w1 & (d0 | d1 | dn);
+        const bool ch = ((n0 ^ x0) | (n1 ^ x1)) != 0ull;
+        x0 = n0;
+        x1 = n1;
+        if (!__any_sync(0xffffffffu, ch)) return true;
+    }
+    return false;
+}
+
+// Writes final = 1 for the weak pixels reached from the tile's seeds and, on
+// success, narrows (f, s) to the union-find's input: unreached components
+// touching the perimeter (f) plus the reached perimeter pixels (f and s).
+// Returns false (f, s untouched) when a fixpoint needed too many rounds.
+__device__ __forceinline__ bool warp_reach(const TileGeo& g, int lane, uint8_t* __restrict__ fin, int W,
+                                           unsigned long long& f0, unsigned long long& f1, unsigned long long& s0,
+                                           unsigned long long& s1) {
+    unsigned long long r0 = s0, r1 = s1;
+    if (!warp_grow(f0, f1, r0, r1, lane)) return false;
+    // perimeter of the valid extent: rows 0 and vh-1 whole, else columns 0 and vw-1
+    const unsigned long long vmask = g.vw == HT ? ~0ull : ((1ull << g.vw) - 1ull);
+    const unsigned long long side = 1ull | (1ull << (g.vw - 1));
+    const int ra = 2 * lane, rb = 2 * lane + 1;
+    const unsigned long long pm0 = (ra == 0 || ra == g.vh - 1) ? vmask : side;
+    const unsigned long long pm1 = (rb == g.vh - 1) ? vmask : side;
+    unsigned long long b0 = f0 & ~r0 & pm0, b1 = f1 & ~r1 & pm1;
+    if (!warp_grow(f0 & ~r0, f1 & ~r1, b0, b1, lane)) return false;
+    // reached pixels are final (weak pixels that join an edge)
+    uint8_t* row0 = fin + (size_t)(g.y0 + ra) * W + g.x0;
+    for (unsigned long long m = r0; m; m &= m - 1) row0[__ffsll((long long)m) - 1] = 1;
+    for (unsigned long long m = r1; m; m &= m - 1) row0[W + __ffsll((long long)m) - 1] = 1;
+    f0 = b0 | (r0 & pm0);
+    f1 = b1 | (r1 & pm1);
+    s0 = r0 & pm0;
+    s1 = r1 & pm1;
+    return true;
+}
+
 // H1: tile-local hysteresis.  Tiles without weak pixels are final as they
 // stand (the final map holds their strong pixels) and export nothing; other
 // tiles run the shared-memory union-find over their weak pixels and append the
@@ -401,13 +501,30 @@ __device__ __forceinline__ void append_node(const HystBufs& b, WsHeader* hdr, lo
 
 __device__ __forceinline__ void hyst_block_tile(const FgBits& B, int H, int W, uint8_t* __restrict__ final_out,
                                                 const HystBufs& b, WsHeader* hdr, long long tile, const TileGeo& g,
-                                                TileCCL& s) {
+                                                TileCCL& s, int reach) {
     const int tid = threadIdx.x;
     const int row = tid >> 1, seg = (tid & 1) * 32;
     if (tid == 0) { s.pending = 0; s.flags = 0; }
-    __syncthreads();
     uint32_t fg, st;  // this thread's weak pixels and their strong-adjacent seeds
+#if EF_H1_REACH
+    // warp 0 loads the tile's rows, runs the tile-local reach (final pixels
+    // written, the union-find input narrowed) and publishes the rows
+    if (tid < 32) {
+        unsigned long long f0, f1, s0, s1;
+        warp_rows(B, g, tid, H, f0, f1, s0, s1);
+        if (reach && __any_sync(0xffffffffu, (f0 | f1) != 0ull))
+            warp_reach(g, tid, final_out + (size_t)g.f * H * W, W, f0, f1, s0, s1);
+        s.fgrow[2 * tid] = f0;
+        s.fgrow[2 * tid + 1] = f1;
+        s.strow[2 * tid] = s0;
+        s.strow[2 * tid + 1] = s1;
+    }
+    __syncthreads();
+    tile_init(s, s.fgrow[tid >> 1], s.strow[tid >> 1], 0ull, false, fg, st);
+#else
+    __syncthreads();
     tile_load(B, H, g, s, fg, st);
+#endif
     __syncthreads();
     const int flags = s.flags;
     const bool general = flags & 1;  // any weak pixel (else the tile is final as it stands)
@@ -495,14 +612,14 @@ __device__ __forceinline__ TileGeo tile_geo_linear(long long tile, int tiles_x, 
 // compact lists hold): one 128-thread block per tile.
 __global__ void __launch_bounds__(H_THREADS)
 hyst_dense_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t* __restrict__ final_out, HystBufs b,
-                  WsHeader* hdr) {
+                  WsHeader* hdr, int reach) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
     const unsigned n = hdr->dense_count;
     for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
         const long long tile = b.dense[e];
-        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s, reach);
     }
 }
 
@@ -582,7 +699,7 @@ __device__ __forceinline__ int row_of(const WarpTile& s, int e) {
 // Grid: (ceil(tiles per frame / WT_WARPS), frames); one warp per tile.
 __global__ void __launch_bounds__(32 * WT_WARPS)
 hyst_local_warp_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t* __restrict__ final_out, HystBufs b,
-                       WsHeader* hdr) {
+                       WsHeader* hdr, int reach) {
     __shared__ WarpTile tiles[WT_WARPS];
     pdl_wait();
     pdl_trigger();
@@ -596,31 +713,28 @@ hyst_local_warp_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t
     const long long tile = (long long)blockIdx.y * tpf + t;
     const int stripe = t % PL_STRIPES;  // == tile % PL_STRIPES only up to the frame offset: any stripe works
     const size_t frame_off = (size_t)g.f * H * W;
-    // rows 2*lane, 2*lane+1: weak pixels (f) and strong pixels (t)
-    const int ya = g.y0 + 2 * lane;
-    const unsigned long long t0 = plane_word(B.st, B, g.f, ya, H, g.txi);
-    const unsigned long long t1 = plane_word(B.st, B, g.f, ya + 1, H, g.txi);
-    const unsigned long long f0 = plane_word(B.fg, B, g.f, ya, H, g.txi) & ~t0;
-    const unsigned long long f1 = plane_word(B.fg, B, g.f, ya + 1, H, g.txi) & ~t1;
-    const bool any_weak = __any_sync(0xffffffffu, (f0 | f1) != 0ull);
-    if (!any_weak) {  // final as it stands (the final map holds its strong pixels); nothing to export
+    // rows 2*lane, 2*lane+1: weak pixels (f) and their seeds (s)
+    unsigned long long f0, f1, s0, s1;
+    warp_rows(B, g, lane, H, f0, f1, s0, s1);
+    if (!__any_sync(0xffffffffu, (f0 | f1) != 0ull)) {  // final as it stands (the final map holds its strong pixels)
         if (lane == 0) {
             b.border[tile] = 0;
             b.pending[tile] = 0;
         }
         return;
     }
-    // seeds: weak pixels 8-adjacent to a strong pixel -- the strong rows above
-    // and below from the neighbouring lanes (the tiles above / below for lanes
-    // 0 and 31), the neighbouring words' edge bits only where a weak pixel sits
-    // at column 0 or 63
-    unsigned long long up = __shfl_up_sync(0xffffffffu, t1, 1), dn = __shfl_down_sync(0xffffffffu, t0, 1);
-    if (lane == 0) up = plane_word(B.st, B, g.f, g.y0 - 1, H, g.txi);
-    if (lane == 31) dn = plane_word(B.st, B, g.f, g.y0 + HT, H, g.txi);
-    const unsigned long long v0 = up | t0 | t1, v1 = t0 | t1 | dn;
-    const unsigned long long s0 = f0 ? f0 & (v0 | (v0 << 1) | (v0 >> 1) | side_strong(B, g.f, ya, H, g.txi, f0)) : 0ull;
-    const unsigned long long s1 =
-        f1 ? f1 & (v1 | (v1 << 1) | (v1 >> 1) | side_strong(B, g.f, ya + 1, H, g.txi, f1)) : 0ull;
+#if EF_H1_REACH
+    // tile-local reach: weak pixels joined to a seed inside the tile are final
+    // now; of the rest only the components touching the perimeter go on
+    if (reach && warp_reach(g, lane, final_out + frame_off, W, f0, f1, s0, s1) &&
+        !__any_sync(0xffffffffu, (f0 | f1) != 0ull)) {
+        if (lane == 0) {
+            b.border[tile] = 0;
+            b.pending[tile] = 0;
+        }
+        return;
+    }
+#endif
     s.fgrow[2 * lane] = f0;
     s.fgrow[2 * lane + 1] = f1;
     s.strow[2 * lane] = s0;
@@ -1037,12 +1151,12 @@ HystLayout hyst_layout(int64_t batch, int H, int W) {
 // each warp walks a large tile's union-find alone.
 __global__ void __launch_bounds__(H_THREADS)
 hyst_all_block_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, long long ntiles,
-                      uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr) {
+                      uint8_t* __restrict__ final_out, HystBufs b, WsHeader* hdr, int reach) {
     __shared__ TileCCL s;
     pdl_wait();
     pdl_trigger();
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s);
+        hyst_block_tile(B, H, W, final_out, b, hdr, tile, tile_geo_linear(tile, tiles_x, tiles_y, H, W), s, reach);
 }
 
 // Label bytes (0/1/2) -> the two foreground bit planes, one thread per 64-bit
@@ -1108,6 +1222,12 @@ static std::atomic<int> g_block_tiles_per_sm{getenv("EF_H1_BLOCK_TILES_PER_SM") 
 
 void set_block_tile_threshold(int tiles_per_sm) { g_block_tiles_per_sm.store(tiles_per_sm); }
 
+// H1's tile-local reach prefilter (ef_set_tile_reach; EF_H1_REACH=0 in the
+// environment starts with it off for measurement runs)
+static std::atomic<int> g_tile_reach{getenv("EF_H1_REACH") ? atoi(getenv("EF_H1_REACH")) : 1};
+
+void set_tile_reach(int on) { g_tile_reach.store(on ? 1 : 0); }
+
 cudaError_t launch_hyst_local(const FgBits& B, int64_t batch, int H, int W, uint8_t* final_out, const HystBufs& b,
                               WsHeader* hdr, int sm_count, cudaStream_t st) {
     HystLayout L = hyst_layout(batch, H, W);
@@ -1127,15 +1247,15 @@ cudaError_t launch_hyst_local(const FgBits& B, int64_t batch, int H, int W, uint
     if (allblock) {
         // few tiles: a block per tile (the dense-tile list stays empty)
         e = launch_pdl(hyst_all_block_kernel, dim3((unsigned)std::min<int64_t>(L.tiles, 16ll * sm_count)),
-                       dim3(H_THREADS), 0, st, B, H, W, L.tiles_x, L.tiles_y, (long long)L.tiles, final_out, b, hdr);
+                       dim3(H_THREADS), 0, st, B, H, W, L.tiles_x, L.tiles_y, (long long)L.tiles, final_out, b, hdr, g_tile_reach.load());
     } else {
         e = launch_pdl(hyst_local_warp_kernel, wgrid, dim3(32 * WT_WARPS), 0, st, B, H, W, L.tiles_x, L.tiles_y,
-                       final_out, b, hdr);
+                       final_out, b, hdr, g_tile_reach.load());
     }
     if (e != cudaSuccess) return e;
     if (!allblock) {  // the block kernel took every tile: the dense list is empty
         e = launch_pdl(hyst_dense_kernel, dim3(sm_count * 4), dim3(H_THREADS), 0, st, B, H, W, L.tiles_x, L.tiles_y,
-                       final_out, b, hdr);
+                       final_out, b, hdr, g_tile_reach.load());
         if (e != cudaSuccess) return e;
     }
     const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);

@@ -150,6 +150,7 @@ cudaError_t launch_band_edges(int rows, int W, const HystBufs& b, const FgBits& 
 cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t* strong_edges,
                               cudaStream_t st);
 void set_block_tile_threshold(int tiles_per_sm);
+void set_tile_reach(int on);
 size_t band_merge_scratch_bytes(int nbands, int W);
 cudaError_t launch_band_merge(int nbands, int W, const int64_t* ids, const uint8_t* strong, uint8_t* out,
                               void* scratch, cudaStream_t st);

@@ -23,14 +23,19 @@ def canny():
     return c
 
 
-@pytest.fixture(params=[0, 32], ids=["warp-per-tile", "block-per-tile-when-few"])
+@pytest.fixture(params=[(0, True), (32, True), (0, False)],
+                ids=["warp-per-tile", "block-per-tile-when-few", "warp-per-tile-no-reach"])
 def h1_path(request, canny):
-    """Both hysteresis tile passes: 0 = always one warp per tile (with the dense
-    tile hand-over), 32 = the default (one block per tile for launches with at
-    most 32 tiles per SM)."""
-    canny.set_block_tile_threshold(request.param)
+    """The hysteresis tile passes: threshold 0 = always one warp per tile (with
+    the dense tile hand-over), 32 = the default (one block per tile for launches
+    with at most 32 tiles per SM); reach = the tile-local reach prefilter before
+    the union-find (default on; off: union-find over every weak pixel)."""
+    thr, reach = request.param
+    canny.set_block_tile_threshold(thr)
+    canny.set_tile_reach(reach)
     yield request.param
     canny.set_block_tile_threshold(32)
+    canny.set_tile_reach(True)
 
 
 def _dev(a):
@@ -181,7 +186,9 @@ def test_dense_noise_overflow_paths(canny, low, high, h1_path):
     # hand-over of tiles with more than 512 weak pixels to the block kernel; at
     # 5 / 100 a third of the pixels are strong and only 0.3% weak
     assert paths["pending_overflow"] == (low < 5.0), paths
-    assert (paths["dense_tiles"] > 0) == (h1_path == 0 and low < 5.0), paths
+    thr, reach = h1_path
+    if not reach:  # with the reach prefilter a tile's union-find input rarely exceeds the warp's lists
+        assert (paths["dense_tiles"] > 0) == (thr == 0 and low < 5.0), paths
     assert np.array_equal(_np(lab), el)
     assert np.array_equal(_np(fin).astype(bool), ef_)
     lab2 = canny.classify_u8(_dev(frames), w, low, high)
