@@ -71,12 +71,6 @@ int ef_set_block_tile_threshold(int32_t tiles_per_sm);
  * over every weak pixel.  The result is identical either way. */
 int ef_set_tile_reach(int32_t on);
 
-/* Classifier tuning: variant 1 (default) = the streaming kernel (one warp per
- * 128-column strip segment of seg_rows output rows; radius <= 4, contiguous
- * sources), 0 = the 32-row tile kernel.  seg_rows 0 keeps the current segment
- * height (default 64).  The result is identical either way. */
-int ef_set_k1_variant(int32_t variant, int32_t seg_rows);
-
 /* Which capacity fallbacks the last call on this workspace took (synchronises
  * `stream`): h_out[0] fix list overflowed (FX scanned every label), [1] a
  * pending-list stripe overflowed (H4 re-ran the pending tiles), [2] tiles H1's

@@ -74,7 +74,6 @@ _SIGNATURES = {
     "ef_read_paths": ([P, SZ, P, P], ctypes.c_int),
     "ef_set_block_tile_threshold": ([I32], ctypes.c_int),
     "ef_set_tile_reach": ([I32], ctypes.c_int),
-    "ef_set_k1_variant": ([I32, I32], ctypes.c_int),
     "ef_band_merge_device": ([I32, I32, P, P, P, P, SZ, P], ctypes.c_int),
     "ef_band_finalize": ([P, I32, I32, P, P, P, SZ, P], ctypes.c_int),
 }

@@ -307,11 +307,6 @@ def set_block_tile_threshold(tiles_per_sm: int) -> None:
     _lib.check(_lib.load().ef_set_block_tile_threshold(int(tiles_per_sm)), "ef_set_block_tile_threshold")
 
 
-def set_k1_variant(variant: int, seg_rows: int = 0) -> None:
-    """Classifier tuning: 1 = streaming kernel (default), 0 = tile kernel; seg_rows > 0 sets the segment height."""
-    _lib.check(_lib.load().ef_set_k1_variant(int(variant), int(seg_rows)), "ef_set_k1_variant")
-
-
 def set_tile_reach(on: bool) -> None:
     """Hysteresis tuning: tile-local reach before the tile union-find (default on)."""
     _lib.check(_lib.load().ef_set_tile_reach(1 if on else 0), "ef_set_tile_reach")

@@ -419,13 +419,6 @@ int ef_set_block_tile_threshold(int32_t tiles_per_sm) {
     return EF_OK;
 }
 
-int ef_set_k1_variant(int32_t variant, int32_t seg_rows) {
-    if (variant != 0 && variant != 1) return fail(EF_EINVAL, "variant must be 0 or 1");
-    if (seg_rows < 0) return fail(EF_EINVAL, "seg_rows must be >= 0");
-    set_k1_variant(variant, seg_rows);
-    return EF_OK;
-}
-
 int ef_set_tile_reach(int32_t on) {
     if (on != 0 && on != 1) return fail(EF_EINVAL, "on must be 0 or 1");
     set_tile_reach(on);

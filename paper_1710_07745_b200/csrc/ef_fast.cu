@@ -173,7 +173,6 @@ k1_classify_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, u
 cudaError_t launch_k1(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
                       uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
                       cudaStream_t st) {
-    if (k1s_selected(P, g)) return launch_k1s(src, batch, g, P, labels, fix_list, hdr, B, st);
     if (k1v2_supported(P, g)) return launch_k1v2(src, batch, g, P, labels, fix_list, hdr, B, st);
     return launch_k1v1(src, batch, g, P, labels, fix_list, hdr, st);
 }

@@ -151,13 +151,7 @@ cudaError_t launch_band_apply(int rows, int W, const HystBufs& b, const uint8_t*
                               cudaStream_t st);
 void set_block_tile_threshold(int tiles_per_sm);
 void set_tile_reach(int on);
-// K1s, the streaming classifier (ef_k1s.cu): selected for contiguous sources
-// where k1v3 runs (radius <= 4) unless ef_set_k1_variant chose the tile kernel
-cudaError_t launch_k1s(const uint8_t* src, int64_t batch, const FrameGeom& g, const FastParams& P,
-                       uint8_t* labels, unsigned long long* fix_list, WsHeader* hdr, const FgBits& B,
-                       cudaStream_t st);
-bool k1s_selected(const FastParams& P, const FrameGeom& g);
-void set_k1_variant(int variant, int seg);
+
 size_t band_merge_scratch_bytes(int nbands, int W);
 cudaError_t launch_band_merge(int nbands, int W, const int64_t* ids, const uint8_t* strong, uint8_t* out,
                               void* scratch, cudaStream_t st);

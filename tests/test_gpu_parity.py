@@ -38,15 +38,6 @@ def h1_path(request, canny):
     canny.set_tile_reach(True)
 
 
-@pytest.fixture(params=[1, 0], ids=["k1-stream", "k1-tile"])
-def k1_variant(request, canny):
-    """Both production classifiers: 1 = the streaming kernel (default for
-    radius <= 4), 0 = the 32-row tile kernel."""
-    canny.set_k1_variant(request.param)
-    yield request.param
-    canny.set_k1_variant(1, 64)
-
-
 def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
@@ -58,7 +49,7 @@ def _np(t):
 # ---------------------------------------------------------------- golden ----
 @pytest.mark.parametrize("cfg", range(5))
 @pytest.mark.parametrize("r", [2, 5])
-def test_configs_match_reference_golden(canny, cfg, r, h1_path, k1_variant):
+def test_configs_match_reference_golden(canny, cfg, r, h1_path):
     g = load("configs.npz")
     frames = synth.make_config(cfg, reduced=True)
     assert synth.sha256_u8(frames) == str(g[f"c{cfg}/sha256"])
@@ -116,7 +107,7 @@ def _random_image(rng, h, w, kind):
 
 
 @pytest.mark.parametrize("r", [0, 1, 2, 3, 4, 5, 6, 7, 8, 15])
-def test_fast_path_random_vs_oracle(canny, r, h1_path, k1_variant):
+def test_fast_path_random_vs_oracle(canny, r, h1_path):
     rng = np.random.default_rng(100 + r)
     sigma = max(0.3, r / 3.0)
     w = O.gaussian_weights(sigma, radius=r)
@@ -131,31 +122,6 @@ def test_fast_path_random_vs_oracle(canny, r, h1_path, k1_variant):
             el, ef_ = O.canny(img, w, low, high)
             assert np.array_equal(_np(lab)[0], el), (r, h, wd, kind, low, high)
             assert np.array_equal(_np(fin)[0].astype(bool), ef_), (r, h, wd, kind, low, high)
-
-
-@pytest.mark.parametrize("r", [1, 2, 3, 4])
-@pytest.mark.parametrize("seg", [1, 5, 64, 4096])
-def test_stream_classifier_segments_vs_oracle(canny, r, seg):
-    """The streaming classifier at segment heights from 1 row (every magnitude
-    row a halo row of its neighbours) to whole frames (long strips: the
-    magnitude ring wraps, rounds forced by the ring), on frames whose strips
-    touch the left / right edges, with sparse and dense candidates."""
-    canny.set_k1_variant(1, seg)
-    try:
-        rng = np.random.default_rng(700 + 10 * r + seg)
-        w = O.gaussian_weights(max(0.3, r / 3.0), radius=r)
-        shapes = [(1, 4), (3, 8), (2, 120), (9, 124), (33, 128), (70, 244), (131, 248), (257, 500), (64, 1024)]
-        for (h, wd) in shapes:
-            for kind in ("noise", "blocks", "ramp"):
-                img = _random_image(rng, h, wd, kind)
-                low = float(rng.choice([0.0, 5.0, 20.0, 100.0]))
-                high = low + float(rng.choice([0.0, 10.0, 40.0, 300.0]))
-                lab, fin = canny.canny_u8(_dev(img), w, low, high)
-                el, ef_ = O.canny(img, w, low, high)
-                assert np.array_equal(_np(lab)[0], el), (r, seg, h, wd, kind, low, high)
-                assert np.array_equal(_np(fin)[0].astype(bool), ef_), (r, seg, h, wd, kind, low, high)
-    finally:
-        canny.set_k1_variant(1, 64)
 
 
 @pytest.mark.parametrize("density", ["sparse", "mixed", "dense"])
@@ -230,7 +196,7 @@ def test_dense_noise_overflow_paths(canny, low, high, h1_path):
 
 
 @pytest.mark.parametrize("low,high", [(48.0, 48.0), (16.0, 48.0)])
-def test_fix_list_overflow_on_threshold_ties(canny, low, high, k1_variant):
+def test_fix_list_overflow_on_threshold_ties(canny, low, high):
     """Binary blocks with a dyadic kernel make magnitudes exactly 16, 48, ...:
     thresholds on those values put ~13% of the pixels inside the certification
     bands (and NMS plateaus), far more than the fix list holds -- the full-scan
