@@ -61,7 +61,7 @@ typedef struct ef_stats {
 
 /* Hysteresis tuning (process-wide): launches with at most tiles_per_sm 64x64
  * tiles per SM run the tile pass with one 128-thread block per tile instead of
- * one warp per tile (few, large tiles: C0, C2).  Default 32; 0 = always one
+ * one warp per tile (few, large tiles: C0).  Default 8; 0 = always one
  * warp per tile.  The result is identical either way. */
 int ef_set_block_tile_threshold(int32_t tiles_per_sm);
 

@@ -1238,9 +1238,9 @@ __global__ void strong_final_kernel(const uint8_t* __restrict__ labels, long lon
 }
 
 // tiles per SM at or below which H1 runs one block per tile (ef_set_block_tile_threshold)
-// (initial value: EF_H1_BLOCK_TILES_PER_SM for measurement runs, else 32)
+// (initial value: EF_H1_BLOCK_TILES_PER_SM for measurement runs, else 8)
 static std::atomic<int> g_block_tiles_per_sm{getenv("EF_H1_BLOCK_TILES_PER_SM") ? atoi(getenv("EF_H1_BLOCK_TILES_PER_SM"))
-                                                                               : 32};
+                                                                               : 8};
 
 void set_block_tile_threshold(int tiles_per_sm) { g_block_tiles_per_sm.store(tiles_per_sm); }
 

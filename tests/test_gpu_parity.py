@@ -27,14 +27,14 @@ def canny():
                 ids=["warp-per-tile", "block-per-tile-when-few", "warp-per-tile-no-reach"])
 def h1_path(request, canny):
     """The hysteresis tile passes: threshold 0 = always one warp per tile (with
-    the dense tile hand-over), 32 = the default (one block per tile for launches
-    with at most 32 tiles per SM); reach = the tile-local reach prefilter before
+    the dense tile hand-over), 32 = one block per tile for launches with at
+    most 32 tiles per SM (the default is 8); reach = the tile-local reach prefilter before
     the union-find (default on; off: union-find over every weak pixel)."""
     thr, reach = request.param
     canny.set_block_tile_threshold(thr)
     canny.set_tile_reach(reach)
     yield request.param
-    canny.set_block_tile_threshold(32)
+    canny.set_block_tile_threshold(8)
     canny.set_tile_reach(True)
 
 

@@ -40,7 +40,7 @@ for thr in (0, 32):
     lab = rng.choice([0, 1, 2], size=(200, 300), p=[0.5, 0.4, 0.1]).astype(np.uint8)
     fin = canny.trace_edges_u8(dev(lab))
     assert np.array_equal(fin.cpu().numpy()[0].astype(bool), O.trace(lab))
-canny.set_block_tile_threshold(32)
+canny.set_block_tile_threshold(8)
 print("trace ok", flush=True)
 blk = rng.choice(np.array([0, 16], np.uint8), size=(64, 64))
 f = np.kron(blk, np.ones((4, 4), np.uint8))[None]
