@@ -429,14 +429,10 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
 __device__ __forceinline__ void warp_rows(const FgBits& B, const TileGeo& g, int lane, int H, unsigned long long& f0,
                                           unsigned long long& f1, unsigned long long& s0, unsigned long long& s1) {
     const int ya = g.y0 + 2 * lane;
-    // this tile's own words: column word txi is always inside the row; rows
-    // past the frame (a partial bottom tile) read as 0
-    const unsigned long long off = (unsigned long long)g.f * B.frame_words + (unsigned long long)ya * B.words + g.txi;
-    const bool in0 = ya < H, in1 = ya + 1 < H;
-    const unsigned long long t0 = in0 ? __ldg(B.st + off) : 0ull;
-    const unsigned long long t1 = in1 ? __ldg(B.st + off + B.words) : 0ull;
-    f0 = (in0 ? __ldg(B.fg + off) : 0ull) & ~t0;
-    f1 = (in1 ? __ldg(B.fg + off + B.words) : 0ull) & ~t1;
+    const unsigned long long t0 = plane_word(B.st, B, g.f, ya, H, g.txi);
+    const unsigned long long t1 = plane_word(B.st, B, g.f, ya + 1, H, g.txi);
+    f0 = plane_word(B.fg, B, g.f, ya, H, g.txi) & ~t0;
+    f1 = plane_word(B.fg, B, g.f, ya + 1, H, g.txi) & ~t1;
     unsigned long long up = __shfl_up_sync(0xffffffffu, t1, 1), dn = __shfl_down_sync(0xffffffffu, t0, 1);
     if (lane == 0) up = plane_word(B.st, B, g.f, g.y0 - 1, H, g.txi);
     if (lane == 31) dn = plane_word(B.st, B, g.f, g.y0 + HT, H, g.txi);
@@ -866,63 +862,45 @@ hyst_local_warp_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t
         }
         return;
     }
-    // lane l owns slots 8l .. 8l+7 (one side of the tile: lanes 0-7 the top
-    // row, 8-15 the bottom row, 16-23 the left column, 24-31 the right
-    // column): the slots' foreground bits come from the row words, node ids
-    // are looked up only where a pixel is foreground, and the 8 entries leave
-    // in two 16-byte stores
-    const int side = lane >> 3, k0 = 8 * (lane & 7);
-    unsigned fgm = 0;  // bit k: slot 8l + k holds a (reduced) weak pixel
-    if (side < 2) {
-        const unsigned long long w = side == 0 ? s.fgrow[0] : s.fgrow[g.vh - 1];
-        fgm = (unsigned)((w & vmask) >> k0) & 0xffu;
-    } else {
-        const int xs = side == 2 ? 0 : g.vw - 1;
+    int nodes[HP / 32];
+    unsigned own[HP / 32];
+    int total = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k0 + k < g.vh) fgm |= (unsigned)((s.fgrow[k0 + k] >> xs) & 1ull) << k;
-    }
-    int node8[8];
-    unsigned ownm = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        node8[k] = -1;
-        if ((fgm >> k) & 1u) {
-            const int p = 8 * lane + k;
-            const int y = side == 0 ? 0 : (side == 1 ? g.vh - 1 : k0 + k);
-            const int x = side == 2 ? 0 : (side == 3 ? g.vw - 1 : k0 + k);
+    for (int j = 0; j < HP / 32; ++j) {
+        const int p = lane + 32 * j;
+        int y, x;
+        slot_pixel(p, g.vh, g.vw, y, x);
+        const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
+        int node = -1;
+        bool mine = false;
+        if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
             const unsigned v = s.info[s.par[cidx(s, y, x)]];
-            node8[k] = (int)(tile * HP) + (int)info_slot(v);
+            node = (int)(tile * HP) + (int)info_slot(v);
             if (info_slot(v) == (unsigned)p) {
-                ownm |= 1u << k;
-                b.gpar[node8[k]] = node8[k];
-                b.gstrong[node8[k]] = info_strong(v) ? 1 : 0;
+                mine = true;
+                b.gpar[node] = node;
+                b.gstrong[node] = info_strong(v) ? 1 : 0;
             }
         }
+        EF_DCHECK(p >= 0 && p < HP && (node < 0 || (node >= tile * HP && node < (tile + 1) * HP)));
+        b.perim[tile * HP + p] = node;
+        nodes[j] = node;
+        own[j] = __ballot_sync(0xffffffffu, mine);
+        total += __popc(own[j]);
     }
-    int4* pdst = reinterpret_cast<int4*>(b.perim + tile * HP + 8 * lane);
-    pdst[0] = make_int4(node8[0], node8[1], node8[2], node8[3]);
-    pdst[1] = make_int4(node8[4], node8[5], node8[6], node8[7]);
-    // own nodes: one append per tile into its node-list stripe
-    const int nown = __popc(ownm);
-    int incl = nown;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total) {
+    if (total) {  // one append per tile into its node-list stripe
         unsigned long long at = 0;
         if (lane == 0) at = atomicAdd(&b.node_count[stripe], (unsigned long long)total);
         at = __shfl_sync(0xffffffffu, at, 0);
         if (at + total > b.node_scap) {
             if (lane == 0) hdr->node_overflow = 1u;
         } else {
-            unsigned long long o = (unsigned long long)stripe * b.node_scap + at + (incl - nown);
+            unsigned long long o = (unsigned long long)stripe * b.node_scap + at;
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((ownm >> k) & 1u) b.node_list[o++] = node8[k];
+            for (int j = 0; j < HP / 32; ++j) {
+                if ((own[j] >> lane) & 1u) b.node_list[o + __popc(own[j] & ((1u << lane) - 1u))] = nodes[j];
+                o += __popc(own[j]);
+            }
         }
     }
     if (lane == 0) {
