@@ -1,4 +1,5 @@
 # hysteresis iteration: suite subset first, then C3 / C1 device bench, launch lists
+python -m paper_1710_07745_b200.build > /dev/null || { echo BUILD FAILED; exit 1; }
 python -c "from oracle import oracle as O; O.build()" > /dev/null
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/t_h.log 2>&1; echo "TESTS: $(tail -1 gpurun_out/t_h.log)"
 grep -E "^E " gpurun_out/t_h.log | head -5

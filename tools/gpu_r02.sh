@@ -2,7 +2,8 @@
 # K1 DRAM bytes on C3, one --set full capture of K1 on C3.
 T=${TAG:-r02}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -m paper_1710_07745_b200.build > /dev/null && python -c "from oracle import oracle as O; O.build()"
+python -m paper_1710_07745_b200.build > /dev/null || { echo BUILD FAILED; exit 1; }
+python -c "from oracle import oracle as O; O.build()"
 timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/t_$T.log 2>&1; echo "TESTS: $(tail -1 gpurun_out/t_$T.log)"
 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke_$T.log 2>&1; tail -1 gpurun_out/smoke_$T.log
 python bench.py > gpurun_out/bench_$T.jsonl 2> gpurun_out/bench_$T.err; echo "BENCH rc=$?"; tail -1 gpurun_out/bench_$T.jsonl
