@@ -1,33 +1,71 @@
-"""Latency of the drop-in run_pipeline on one 1080p frame (float64 GrayImage in,
-host EdgeMap out), default radius (ceil(3 sigma) = 5) and the configs' 5x5."""
-import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
-import paper_1710_07745_b200 as ef
-from paper_1710_07745_b200 import synth
+"""Latency of the drop-in run_pipeline (float64 GrayImage in, host EdgeMap out)
+against the reference's own run_pipeline on the same host, for one 512x512
+frame (config 0) and one 1080p frame (a config-1 frame): the reference's
+default kernel (radius ceil(3 sigma) = 5), thresholds 20 / 50.  The results
+are compared for equality (labels and final).  Run on the GPU box:
 
-frame = synth.make_config(1)[0].astype(np.float64)
-img = ef.GrayImage.from_array(frame) if hasattr(ef.GrayImage, "from_array") else ef.GrayImage(frame.shape[1], frame.shape[0], frame)
-for radius in (None, 2):
-    cfg = ef.PipelineConfig(sigma=1.4, thresholds=ef.Thresholds(20.0, 50.0), radius=radius)
-    for _ in range(3):
-        ef.run_pipeline(img, cfg)
-    t0 = time.perf_counter()
-    n = 20
-    for _ in range(n):
-        res = ef.run_pipeline(img, cfg)
-    dt = (time.perf_counter() - t0) / n
-    print(f"radius {radius}: {dt * 1e3:.2f} ms per 1080p frame ({frame.size / dt / 1e6:.0f} MP/s)")
+    python tools/dropin_latency.py [--json out.json]
 
-# breakdown
-from paper_1710_07745_b200 import canny
-from paper_1710_07745_b200.filtering import build_gaussian_kernel
-w = build_gaussian_kernel(1.4).weights
-t0 = time.perf_counter()
-for _ in range(20):
-    u8 = img.as_u8()
-t1 = time.perf_counter()
-for _ in range(20):
-    canny.canny_u8_host(u8, w, 20.0, 50.0)
-t2 = time.perf_counter()
-print(f"as_u8 {(t1 - t0) / 20 * 1e3:.2f} ms, canny_u8_host {(t2 - t1) / 20 * 1e3:.2f} ms")
+The reference is imported from baseline/_ref (its unmodified install); without
+it only this package is timed.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_1710_07745_b200 as ef  # noqa: E402
+from paper_1710_07745_b200 import synth  # noqa: E402
+
+
+def timed(fn, reps, warm=2):
+    for _ in range(warm):
+        out = fn()
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        t.append(time.perf_counter() - t0)
+    return float(np.median(t)), out
+
+
+def main():
+    ref = None
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "edgeforge")):
+        sys.path.insert(0, ref_dir)
+        import edgeforge as ref  # the reference, unmodified
+    cores = len(os.sched_getaffinity(0))
+    frames = {"C0 512x512": np.asarray(synth.make_config(0)).reshape(512, 512),
+              "C1 frame 0 (1080p)": np.asarray(synth.config1_frame(0)).reshape(1080, 1920)}
+    rows = []
+    for name, f in frames.items():
+        f64 = np.ascontiguousarray(f, dtype=np.float64)
+        img = ef.GrayImage.from_array(f64)
+        cfg = ef.PipelineConfig(sigma=1.4, thresholds=ef.Thresholds(20.0, 50.0))
+        ours_s, res = timed(lambda: ef.run_pipeline(img, cfg), 20)
+        row = {"frame": name, "pixels": int(f.size), "ours_ms": round(ours_s * 1e3, 3)}
+        if ref is not None:
+            rimg = ref.GrayImage.from_array(f64)
+            rcfg = ref.PipelineConfig(sigma=1.4, thresholds=ref.Thresholds(20.0, 50.0),
+                                      workers=ref.WorkerConfig(workers=cores))
+            ref_s, rres = timed(lambda: ref.run_pipeline(rimg, rcfg), 3, warm=1)
+            row.update({"reference_ms": round(ref_s * 1e3, 3), "reference_workers": cores,
+                        "speedup": round(ref_s / ours_s, 1),
+                        "labels_equal": bool(np.array_equal(np.asarray(res.edges.labels),
+                                                            np.asarray(rres.edges.labels))),
+                        "final_equal": bool(np.array_equal(np.asarray(res.edges.final),
+                                                           np.asarray(rres.edges.final)))})
+        rows.append(row)
+        print(json.dumps(row))
+    if "--json" in sys.argv:
+        with open(sys.argv[sys.argv.index("--json") + 1], "w") as fh:
+            json.dump(rows, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
