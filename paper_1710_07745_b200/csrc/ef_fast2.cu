@@ -42,6 +42,13 @@
 
 namespace ef {
 
+#ifdef EF_DEBUG_DUMP
+struct DbgDump {
+    float *m2, *gx, *gy;
+};
+__device__ DbgDump g_dbg = {nullptr, nullptr, nullptr};
+#endif
+
 #ifndef EF_K1_WARPS
 #define EF_K1_WARPS 4
 #endif
@@ -460,6 +467,16 @@ __device__ __forceinline__ void v3_phase2a(const FrameGeom& g, int xv0, int y0, 
         const float2 gy23 = add2(f2(sm[pd][2], sm[pd][3]), f2(-sm[pu][2], -sm[pu][3]));
         float2 m01 = fma2(gx01, gx01, mul2(gy01, gy01));
         float2 m23 = fma2(gx23, gx23, mul2(gy23, gy23));
+#ifdef EF_DEBUG_DUMP
+        // certification-margin study (tools/cert_margin.py): the fp32 squared
+        // magnitude and gradient of every output pixel, as the classifier sees them
+        if (g_dbg.m2 && j >= 1 && j <= V2_TH && out_lane && Ym < ylim) {
+            const unsigned long long o = O.out_base + (unsigned long long)(Ym - g.out0) * W + c;
+            *reinterpret_cast<float4*>(g_dbg.m2 + o) = make_float4(m01.x, m01.y, m23.x, m23.y);
+            *reinterpret_cast<float4*>(g_dbg.gx + o) = make_float4(gx01.x, gx01.y, gx23.x, gx23.y);
+            *reinterpret_cast<float4*>(g_dbg.gy + o) = make_float4(gy01.x, gy01.y, gy23.x, gy23.y);
+        }
+#endif
         EF_DCHECK(j >= 0 && j < V3_MROWS);
         *reinterpret_cast<float4*>(&S.m[j][4 * lane]) = make_float4(m01.x, m01.y, m23.x, m23.y);
         // output rows: groups certainly below `low` get the background class
@@ -671,6 +688,16 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
+
+#ifdef EF_DEBUG_DUMP
+// debug builds only (-DEF_DEBUG_DUMP): K1 stores its fp32 m^2 / gx / gy of every
+// output pixel into these device buffers (one float per pixel, label layout;
+// 16-byte aligned); nullptr turns it off
+extern "C" int ef_debug_dump(float* m2, float* gx, float* gy) {
+    DbgDump d{m2, gx, gy};
+    return cudaMemcpyToSymbol(g_dbg, &d, sizeof d) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // the production classifier reads the source and writes labels / final in
 // 32-bit words: every caller buffer 4-byte aligned (P.no_v2 == 0), W % 4 == 0
