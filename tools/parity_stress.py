@@ -1,0 +1,70 @@
+"""Extended parity sweep (beyond tests/): the fused CUDA path against the CPU
+oracle on many seeded random images -- sizes, radii, sigmas, thresholds and
+content kinds drawn at random -- plus full C1 at the reference's default radius
+5.  Prints one JSON line per group and exits non-zero on the first mismatch.
+
+    python tools/parity_stress.py [--n 300] [--seed 11]
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402  (the checker)
+from paper_1710_07745_b200 import canny, synth  # noqa: E402
+
+
+def image(rng, h, w, kind):
+    if kind == "noise":
+        return rng.integers(0, 256, (h, w), dtype=np.uint8)
+    if kind == "smooth_noise":  # low-contrast texture: many near-threshold magnitudes
+        base = rng.normal(128, 6, (h, w))
+        return np.clip(np.round(base), 0, 255).astype(np.uint8)
+    if kind == "blocks":
+        b = rng.integers(0, 256, (h // 5 + 1, w // 5 + 1))
+        return np.kron(b, np.ones((5, 5)))[:h, :w].astype(np.uint8)
+    y, x = np.mgrid[0:h, 0:w]
+    a, c = rng.integers(1, 9, 2)
+    return ((x * a + y * c) % 256).astype(np.uint8)
+
+
+def main():
+    n = int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 300
+    seed = int(sys.argv[sys.argv.index("--seed") + 1]) if "--seed" in sys.argv else 11
+    rng = np.random.default_rng(seed)
+    checked = 0
+    for i in range(n):
+        h = int(rng.integers(1, 700))
+        w = int(rng.integers(1, 900))
+        r = int(rng.integers(0, 9))
+        sigma = float(rng.uniform(0.3, 3.0))
+        kind = str(rng.choice(["noise", "smooth_noise", "blocks", "ramp"]))
+        low = float(rng.choice([0.0, 1.0, 5.0, 10.0, 20.0, 40.0, 100.0]))
+        high = low + float(rng.choice([0.0, 2.0, 10.0, 30.0, 200.0]))
+        img = image(rng, h, w, kind)
+        wts = O.gaussian_weights(sigma, radius=r)
+        lab, fin = canny.canny_u8(torch.from_numpy(img).cuda(), wts, low, high)
+        el, ef = O.canny(img, wts, low, high)
+        ok = np.array_equal(lab.cpu().numpy()[0], el) and np.array_equal(fin.cpu().numpy()[0].astype(bool), ef)
+        checked += img.size
+        if not ok:
+            print(json.dumps({"mismatch": {"i": i, "h": h, "w": w, "r": r, "sigma": sigma, "kind": kind,
+                                           "low": low, "high": high}}))
+            sys.exit(1)
+    print(json.dumps({"group": "random", "images": n, "pixels": checked, "seed": seed, "mismatches": 0}))
+    # full C1 (64 x 1080p) at the reference's default kernel (radius 5)
+    frames = synth.config_range(1, 0, 64)
+    wts = O.gaussian_weights(1.4)
+    lab, fin = canny.canny_u8(torch.from_numpy(frames).cuda(), wts, 20.0, 50.0)
+    el, ef = O.canny(frames, wts, 20.0, 50.0)
+    ok = np.array_equal(lab.cpu().numpy(), el) and np.array_equal(fin.cpu().numpy().astype(bool), ef)
+    print(json.dumps({"group": "C1 64 frames radius 5", "pixels": int(frames.size), "mismatches": 0 if ok else 1}))
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
