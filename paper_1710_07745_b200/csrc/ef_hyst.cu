@@ -418,6 +418,7 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
 #ifndef EF_H1_REACH
 #define EF_H1_REACH 1
 #endif
+
 #ifndef EF_H1_REACH_ITERS
 #define EF_H1_REACH_ITERS 48
 #endif
@@ -865,15 +866,26 @@ hyst_local_warp_kernel(FgBits B, int H, int W, int tiles_x, int tiles_y, uint8_t
     int nodes[HP / 32];
     unsigned own[HP / 32];
     int total = 0;
+    // the 8 slots' foreground bits from registers: the top / bottom row words
+    // (broadcast loads) and this lane's rows lane, lane + 32 (their column 0 /
+    // vw-1 bits); only foreground slots look their component up
+    unsigned pfg = 0;
+    {
+        const unsigned long long top = s.fgrow[0] & vmask, bot = s.fgrow[g.vh - 1] & vmask;
+        const unsigned long long ra = s.fgrow[lane], rb = s.fgrow[lane + 32];
+        pfg |= (unsigned)((top >> lane) & 1ull) | (unsigned)((top >> (lane + 32)) & 1ull) << 1;
+        pfg |= (unsigned)((bot >> lane) & 1ull) << 2 | (unsigned)((bot >> (lane + 32)) & 1ull) << 3;
+        pfg |= (unsigned)(ra & 1ull) << 4 | (unsigned)(rb & 1ull) << 5;  // rows >= vh hold no foreground
+        pfg |= (unsigned)((ra >> (g.vw - 1)) & 1ull) << 6 | (unsigned)((rb >> (g.vw - 1)) & 1ull) << 7;
+    }
 #pragma unroll
     for (int j = 0; j < HP / 32; ++j) {
         const int p = lane + 32 * j;
-        int y, x;
-        slot_pixel(p, g.vh, g.vw, y, x);
-        const bool valid = (p < 128) ? (x < g.vw) : (y < g.vh);
         int node = -1;
         bool mine = false;
-        if (valid && y >= 0 && x >= 0 && ((s.fgrow[y] >> x) & 1ull)) {
+        if ((pfg >> j) & 1u) {  // a foreground pixel at the slot (the valid extent is in the masks)
+            int y, x;
+            slot_pixel(p, g.vh, g.vw, y, x);
             const unsigned v = s.info[s.par[cidx(s, y, x)]];
             node = (int)(tile * HP) + (int)info_slot(v);
             if (info_slot(v) == (unsigned)p) {
