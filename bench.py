@@ -440,13 +440,17 @@ def measure_e2e(frames, weights, low, high, steps, dev, world):
                                 dev.index)
     _barrier(world)
     e_steps = max(3, min(steps, 10))
+    per = []
     t0 = time.perf_counter()
     for _ in range(e_steps):
+        t1 = time.perf_counter()
         canny.canny_u8_host_ptr(hsrc.data_ptr(), b, h, wd, weights, low, high, hlab.data_ptr(), hfin.data_ptr(),
                                 dev.index)
+        per.append((time.perf_counter() - t1) * 1e3)
     e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
     e_ms = _max_over_ranks(e_ms, dev, world)
-    return e_ms, e_steps
+    spread = {"min": round(min(per), 3), "median": round(statistics.median(per), 3), "max": round(max(per), 3)}
+    return e_ms, e_steps, spread
 
 
 def measure_bands(frame_rank0, weights, low, high, steps, warmup, dev, rank, world, peer=False):
@@ -577,9 +581,10 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e_ms, e_steps = measure_e2e(frames, w, low, high, args.steps, dev, world)
+        e_ms, e_steps, spread = measure_e2e(frames, w, low, high, args.steps, dev, world)
         e2e = {"value": round(total_px / 1e6 / (e_ms / 1e3), 3), "unit": "MP/s", "ms_per_step": round(e_ms, 3),
-               "steps": e_steps, "h2d_bytes_per_step": int(total_px), "d2h_bytes_per_step": int(world * -(-px // 4)),
+               "steps": e_steps, "step_ms_rank0": spread,
+               "h2d_bytes_per_step": int(total_px), "d2h_bytes_per_step": int(world * -(-px // 4)),
                "path": "ef_canny_u8_host per rank (pinned input; 3-stream chunked copy/compute overlap; labels+final "
                        "cross PCIe packed to 2 bits/px and are expanded into the host arrays by a host thread pool); "
                        "wall clock, max over ranks"}
