@@ -585,21 +585,25 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
 // in shared memory by replicating their edge rows / columns (np.pad edge at
 // every stage, the reference's border policy) -- after which the interior code
 // runs unchanged.  Columns first, then rows (corners = corner pixel).
+// [c_use0, c_use1]: the columns the phases read (the staged input box is up
+// to 16 columns wider than the tile's 128 on the left, for TMA's 16-byte box
+// alignment: those margin columns are never read and are not filled)
 template <int NROWS, int NCOLS, int STRIDE, class T>
-__device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_hi, int r_lo, int r_hi) {
+__device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_hi, int r_lo, int r_hi,
+                                                int c_use0 = 0, int c_use1 = NCOLS - 1) {
     auto at = [&](int r, int c) -> T& { return a[r][c]; };  // (NCOLS logical columns of STRIDE)
     // only the out-of-frame margins are touched: one row per thread, then one
     // column per thread
-    if (c_lo > 0 || c_hi < NCOLS - 1) {
+    if (c_lo > c_use0 || c_hi < c_use1) {
         for (int r = threadIdx.x; r < NROWS; r += blockDim.x) {
             const T vl = at(r, c_lo), vr = at(r, c_hi);
-            for (int c = 0; c < c_lo; ++c) at(r, c) = vl;
-            for (int c = c_hi + 1; c < NCOLS; ++c) at(r, c) = vr;
+            for (int c = c_use0; c < c_lo; ++c) at(r, c) = vl;
+            for (int c = c_hi + 1; c <= c_use1; ++c) at(r, c) = vr;
         }
         __syncthreads();
     }
     if (r_lo > 0 || r_hi < NROWS - 1) {
-        for (int c = threadIdx.x; c < NCOLS; c += blockDim.x) {
+        for (int c = c_use0 + threadIdx.x; c <= c_use1; c += blockDim.x) {
             const T vt = at(r_lo, c), vb = at(r_hi, c);
             for (int r = 0; r < r_lo; ++r) at(r, c) = vt;
             for (int r = r_hi + 1; r < NROWS; ++r) at(r, c) = vb;
@@ -650,7 +654,8 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
                 replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
-                                                 max(0, ylo - yin), min(NIN - 1, yhi - yin));
+                                                 max(0, ylo - yin), min(NIN - 1, yhi - yin), xv0 - xa,
+                                                 xv0 - xa + V2_COLS - 1);
             }
         } else {
             // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
