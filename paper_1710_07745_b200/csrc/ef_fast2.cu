@@ -653,9 +653,11 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             tma_wait(S);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
-                replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
-                                                 max(0, ylo - yin), min(NIN - 1, yhi - yin), xv0 - xa,
-                                                 xv0 - xa + V2_COLS - 1);
+                // only the input columns within R of the frame feed an in-frame blurred value
+                const int cl = max(0, -xa), ch = min(V2_IN_COLS - 1, W - 1 - xa);
+                replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, cl, ch, max(0, ylo - yin), min(NIN - 1, yhi - yin),
+                                                             max(xv0 - xa, cl - R),
+                                                             min(xv0 - xa + V2_COLS - 1, ch + R));
             }
         } else {
             // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
@@ -683,13 +685,17 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     v2_phase1<R>(xv0, y0, P, S, warp, lane);
     __syncthreads();
     if (!interior)  // blurred: row i <-> frame row y0-2+i, column c <-> x = xv0 + c
+        // blurred and magnitude values are read at most one column past the
+        // frame (Sobel and NMS neighbours of the edge columns)
         replicate_edges<V2_BROWS, V2_COLS, V2_CS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                           max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)));
+                                                  max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)),
+                                                  max(0, -xv0 - 1), min(V2_COLS - 1, W - xv0));
     v3_phase2a<R, FUSED>(g, xv0, y0, P, S, warp, lane, O);
     __syncthreads();
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS, V2_CS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                           max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)));
+                                                  max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)),
+                                                  max(0, -xv0 - 1), min(V2_COLS - 1, W - xv0));
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
