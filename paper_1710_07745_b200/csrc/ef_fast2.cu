@@ -585,31 +585,36 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
 // in shared memory by replicating their edge rows / columns (np.pad edge at
 // every stage, the reference's border policy) -- after which the interior code
 // runs unchanged.  Columns first, then rows (corners = corner pixel).
-// [c_use0, c_use1]: the columns the phases read (the staged input box is up
-// to 16 columns wider than the tile's 128 on the left, for TMA's 16-byte box
-// alignment: those margin columns are never read and are not filled)
+// Only the margin the next stage reads is filled: `marg` columns / rows past
+// the in-frame range [c_lo, c_hi] x [r_lo, r_hi] (R for the staged input, whose
+// blurred values feed the in-frame columns; 1 for the blurred and magnitude
+// tiles, read by the Sobel / NMS neighbours of the edge pixels), and never the
+// staged box's alignment margin outside [c_use0, c_use1].  The out-of-frame
+// rows copy the edge row at the CLAMPED column, so the column and row passes
+// are independent: one barrier.
 template <int NROWS, int NCOLS, int STRIDE, class T>
-__device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_hi, int r_lo, int r_hi,
+__device__ __forceinline__ void replicate_edges(T (*a)[STRIDE], int c_lo, int c_hi, int r_lo, int r_hi, int marg,
                                                 int c_use0 = 0, int c_use1 = NCOLS - 1) {
     auto at = [&](int r, int c) -> T& { return a[r][c]; };  // (NCOLS logical columns of STRIDE)
-    // only the out-of-frame margins are touched: one row per thread, then one
-    // column per thread
-    if (c_lo > c_use0 || c_hi < c_use1) {
-        for (int r = threadIdx.x; r < NROWS; r += blockDim.x) {
+    const int c0 = max(c_use0, c_lo - marg), c1 = min(c_use1, c_hi + marg);
+    const int r0 = max(0, r_lo - marg), r1 = min(NROWS - 1, r_hi + marg);
+    const bool cols = c0 < c_lo || c1 > c_hi, rows = r0 < r_lo || r1 > r_hi;  // block-uniform
+    if (cols) {  // in-frame rows: one row per thread
+        for (int r = r_lo + threadIdx.x; r <= r_hi; r += blockDim.x) {
             const T vl = at(r, c_lo), vr = at(r, c_hi);
-            for (int c = c_use0; c < c_lo; ++c) at(r, c) = vl;
-            for (int c = c_hi + 1; c <= c_use1; ++c) at(r, c) = vr;
+            for (int c = c0; c < c_lo; ++c) at(r, c) = vl;
+            for (int c = c_hi + 1; c <= c1; ++c) at(r, c) = vr;
         }
-        __syncthreads();
     }
-    if (r_lo > 0 || r_hi < NROWS - 1) {
-        for (int c = c_use0 + threadIdx.x; c <= c_use1; c += blockDim.x) {
-            const T vt = at(r_lo, c), vb = at(r_hi, c);
-            for (int r = 0; r < r_lo; ++r) at(r, c) = vt;
-            for (int r = r_hi + 1; r < NROWS; ++r) at(r, c) = vb;
+    if (rows) {  // out-of-frame rows: one column per thread, the edge row at the clamped column
+        for (int c = c0 + threadIdx.x; c <= c1; c += blockDim.x) {
+            const int cs = min(max(c, c_lo), c_hi);
+            const T vt = at(r_lo, cs), vb = at(r_hi, cs);
+            for (int r = r0; r < r_lo; ++r) at(r, c) = vt;
+            for (int r = r_hi + 1; r <= r1; ++r) at(r, c) = vb;
         }
-        __syncthreads();
     }
+    if (cols || rows) __syncthreads();
 }
 
 template <int R, bool FUSED, bool PEER = false>
@@ -653,11 +658,9 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
             tma_wait(S);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
                 __syncthreads();
-                // only the input columns within R of the frame feed an in-frame blurred value
-                const int cl = max(0, -xa), ch = min(V2_IN_COLS - 1, W - 1 - xa);
-                replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, cl, ch, max(0, ylo - yin), min(NIN - 1, yhi - yin),
-                                                             max(xv0 - xa, cl - R),
-                                                             min(xv0 - xa + V2_COLS - 1, ch + R));
+                replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
+                                                             max(0, ylo - yin), min(NIN - 1, yhi - yin), R,
+                                                             xv0 - xa, xv0 - xa + V2_COLS - 1);
             }
         } else {
             // no TMA (W % 16 != 0 or an unaligned buffer): 4-byte loads (W % 4 == 0),
@@ -688,14 +691,12 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         // blurred and magnitude values are read at most one column past the
         // frame (Sobel and NMS neighbours of the edge columns)
         replicate_edges<V2_BROWS, V2_COLS, V2_CS>(S.b, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                                  max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)),
-                                                  max(0, -xv0 - 1), min(V2_COLS - 1, W - xv0));
+                                                  max(0, -(y0 - 2)), min(V2_BROWS - 1, FH - 1 - (y0 - 2)), 1);
     v3_phase2a<R, FUSED>(g, xv0, y0, P, S, warp, lane, O);
     __syncthreads();
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS, V2_CS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
-                                                  max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)),
-                                                  max(0, -xv0 - 1), min(V2_COLS - 1, W - xv0));
+                                                  max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)), 1);
     const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
