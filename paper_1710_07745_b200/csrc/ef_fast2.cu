@@ -657,7 +657,7 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
         if (tma_tile) {
             tma_wait(S);
             if (!interior) {  // the box read zeros outside the buffer: replicate the edges
-                __syncthreads();
+                // (every thread has waited on the mbarrier itself: the box is visible, no barrier first)
                 replicate_edges<NIN, V2_IN_COLS, V2_IN_COLS>(S.in, max(0, -xa), min(V2_IN_COLS - 1, W - 1 - xa),
                                                              max(0, ylo - yin), min(NIN - 1, yhi - yin), R,
                                                              xv0 - xa, xv0 - xa + V2_COLS - 1);
