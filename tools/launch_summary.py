@@ -12,7 +12,8 @@ for path in sys.argv[1:]:
     ik, iv = h.index("Kernel Name"), h.index("Metric Value")
     d = collections.OrderedDict()
     for r in rows[1:]:
-        k = r[ik].split("(")[0].split("<")[0].replace("void ", "").replace("ef::", "") or "(memset/other)"
+        name = r[ik].replace("void ", "").replace("ef::", "").replace("<unnamed>::", "")
+        k = name.split("(")[0].split("<")[0] or "(memset/other)"
         d.setdefault(k, []).append(float(r[iv]))
     print("==", path)
     for k, v in d.items():
