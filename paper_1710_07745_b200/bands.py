@@ -262,6 +262,22 @@ def ipc_open(handle: bytes, offset: int) -> tuple[int, int]:
     return int(ptr.value), int(base.value)
 
 
+def _gather_stacked(tensor, world, group):
+    """Every rank's `tensor` stacked along a new first axis: one band needs no
+    collective; NCCL gathers straight into the stacked buffer (no per-rank
+    list, no stacking copy); gloo goes through _gather."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return tensor.unsqueeze(0)
+    if tensor.is_cuda and dist.get_backend(group) == "nccl":
+        out = torch.empty((world,) + tuple(tensor.shape), dtype=tensor.dtype, device=tensor.device)
+        dist.all_gather_into_tensor(out, tensor.contiguous(), group=group)
+        return out
+    return torch.stack(_gather(tensor, world, group))
+
+
 def _gather(tensor, world, group):
     """all_gather that also works for CUDA tensors under gloo (host staging)."""
     import torch
@@ -401,9 +417,11 @@ def _merge_and_finalize(be, band_u8, rank, world, group):
 
     w = band_u8.shape[1]
     ids, strong = be.edges()
+    if world == 1:  # one band: no seams; every edge entry keeps its own component's flag
+        return be.labels, be.finalize(strong)
     if hasattr(be, "merge"):
         # device path: gather the edge rows device to device, merge on the device
-        merged = be.merge(torch.stack(_gather(ids, world, group)), torch.stack(_gather(strong, world, group)))
+        merged = be.merge(_gather_stacked(ids, world, group), _gather_stacked(strong, world, group))
         return be.labels, be.finalize(merged[rank])
     # host path (backends without a device merge): globalised ids, host union-find
     gids = torch.from_numpy(globalize_ids(ids.cpu().numpy(), rank)).to(band_u8.device)
