@@ -960,7 +960,12 @@ __device__ __forceinline__ void seam_unite(int* gpar, int a0, int a1, int c0, in
 // loads are issued before any union (one round trip, not two), and runs of
 // one component along a seam unite once.  Perimeter slots outside the valid
 // extent hold -1.
-__global__ void __launch_bounds__(256)
+#ifndef EF_H2_WARPS
+#define EF_H2_WARPS 8
+#endif
+constexpr int H2_WARPS = EF_H2_WARPS;  // tiles (warps) per merge block
+
+__global__ void __launch_bounds__(32 * H2_WARPS)
 hyst_merge_kernel(int H, int W, int tiles_x, int tiles_y, HystBufs b) {
     pdl_wait();
     pdl_trigger();
@@ -1275,8 +1280,8 @@ cudaError_t launch_hyst_local(const FgBits& B, int64_t batch, int H, int W, uint
                        final_out, b, hdr, g_tile_reach.load());
         if (e != cudaSuccess) return e;
     }
-    const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + 7) / 8), (unsigned)batch);
-    e = launch_pdl(hyst_merge_kernel, mgrid, dim3(256), 0, st, H, W, L.tiles_x, L.tiles_y, b);
+    const dim3 mgrid((unsigned)((L.tiles_x * L.tiles_y + H2_WARPS - 1) / H2_WARPS), (unsigned)batch);
+    e = launch_pdl(hyst_merge_kernel, mgrid, dim3(32 * H2_WARPS), 0, st, H, W, L.tiles_x, L.tiles_y, b);
     if (e != cudaSuccess) return e;
     return launch_pdl(hyst_resolve_kernel, dim3(stripe_blocks(L.tiles, sm_count), PL_STRIPES), dim3(256), 0, st,
                       (long long)L.slots, b, hdr);
