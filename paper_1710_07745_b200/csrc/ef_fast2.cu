@@ -239,10 +239,23 @@ __device__ __forceinline__ void load6(const float* row, int cc0, float (&v)[6]) 
     v[5] = row[cc0 + 4];
 }
 
+// The tile's output addresses, formed once per thread before the classifier's
+// rounds (per group: 32-bit row / column offsets from these bases; forming the
+// 64-bit label, final and bit-plane addresses from the frame geometry in every
+// round cost ~30 instructions of ~330).
+struct V2Dst {
+    unsigned long long lab0;  // label index of (tile row 0, column xv0)
+    uint8_t* lab;             // labels + lab0
+    long long fin_off;        // final map - label map (bytes)
+    unsigned long long* fg;   // bit-plane words of tile row 0
+    unsigned long long* st;
+    int words;                // words per output row
+};
+
 template <bool FUSED>
-__device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Yc, int cl, const float* mu,
+__device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int j, int cl, const float* mu,
                                                   const float* mc, const float* md, const float* bu,
-                                                  const float* bm, const float* bd, const FgBits& bits,
+                                                  const float* bm, const float* bd, const V2Dst& D,
                                                   const V2Out& O) {
     const float t1 = 0.41421356237309503f;
     const int cc0 = 4 * cl;
@@ -286,7 +299,7 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
         any_flag |= flag;
         packed |= lab << (8 * k);
     }
-    const unsigned long long rowbase = O.out_base + (unsigned long long)(Yc - P.out0) * P.W;
+    const unsigned off = (unsigned)j * (unsigned)P.W + (unsigned)cc0;  // from (tile row 0, column xv0)
     if (any_flag) {
         // one list append per group (global-space ops: see fg_bits_or)
         unsigned fm = 0, cnt = 0;
@@ -303,7 +316,7 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
             if (!((fm >> k) & 1u)) continue;
             if (slot < cap)
                 asm volatile("st.global.u64 [%0], %1;" ::"l"(O.fix_list + slot),
-                             "l"(rowbase + (unsigned long long)(xv0 + cc0 + k)) : "memory");
+                             "l"(D.lab0 + off + (unsigned long long)k) : "memory");
             else
                 st_global_u32(&O.hdr->overflow, 1u);
             ++slot;
@@ -311,17 +324,25 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int Y
     }
     EF_DCHECK(cc0 >= 4 && cc0 + 4 < V2_CS && xv0 + cc0 >= 0 && xv0 + cc0 + 4 <= P.W);
 #ifdef EF_DEBUG_CHECKS
-    EF_DCHECK(rowbase + xv0 + cc0 + 4 <= O.npx);
+    EF_DCHECK(D.lab0 + off + 4 <= O.npx);
 #endif
-    st_global_u32(O.labels + rowbase + xv0 + cc0, packed);
+    uint8_t* const lp = D.lab + off;
+    st_global_u32(lp, packed);
     if (FUSED) {
         // final = strong (kFlag bytes give 0: the fix-up writes them)
-        st_global_u32(O.labels + rowbase + xv0 + cc0 + bits.fin_off, (packed >> 1) & 0x01010101u);
+        st_global_u32(lp + D.fin_off, (packed >> 1) & 0x01010101u);
         // bytes are 0, 1, 2 or kFlag (0x80, resolved by the fix-up, which sets its own bits)
         const uint32_t lo = packed & 0x03030303u;
         const uint32_t fgn = (((lo | (lo >> 1)) & 0x01010101u) * 0x10204080u) >> 28;
         const uint32_t stn = (((packed >> 1) & 0x01010101u) * 0x10204080u) >> 28;
-        if (fgn) fg_bits_or(bits, blockIdx.z, Yc - P.out0, xv0 + cc0, fgn, stn);
+        const int x = xv0 + cc0;
+        const unsigned w = (unsigned)j * (unsigned)D.words + (unsigned)(x >> 6);
+        EF_DCHECK((x & 3) == 0 && (unsigned)(x >> 6) < (unsigned)D.words);
+        // global-space reductions (see fg_bits_or)
+        if (fgn)
+            asm volatile("red.global.or.b64 [%0], %1;" ::"l"(D.fg + w), "l"((unsigned long long)fgn << (x & 63)) : "memory");
+        if (stn)
+            asm volatile("red.global.or.b64 [%0], %1;" ::"l"(D.st + w), "l"((unsigned long long)stn << (x & 63)) : "memory");
     }
 }
 
@@ -556,6 +577,18 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     constexpr int NW2 = NW <= 1 ? 1 : (NW <= 2 ? 2 : (NW <= 4 ? 4 : (NW <= 8 ? 8 : (NW <= 16 ? 16 : 32))));
+    if (first >= total) return;
+    V2Dst D;
+    D.lab0 = O.out_base + (unsigned long long)(y0 - P.out0) * (unsigned)P.W + (unsigned long long)xv0;
+    D.lab = O.labels + D.lab0;
+    D.fin_off = FUSED ? S.bits.fin_off : 0;
+    D.words = FUSED ? S.bits.words : 0;
+    D.fg = D.st = nullptr;
+    if (FUSED) {
+        const unsigned long long w0 = blockIdx.z * S.bits.frame_words + (unsigned long long)(y0 - P.out0) * S.bits.words;
+        D.fg = S.bits.fg + w0;
+        D.st = S.bits.st + w0;
+    }
     for (int base = first; base < total; base += stride) {
         const int k = base + lane;
         int i = 0;  // first word whose inclusive count exceeds k
@@ -574,8 +607,8 @@ __device__ __forceinline__ void v3_classify(const V2Cls P, int xv0, int y0, V3Sm
 #endif
             EF_DCHECK(j >= 0 && j + 2 < V3_MROWS && j + 3 < V2_BROWS && i >= 0 && i < NW);
             EF_DCHECK(select32(w, k - before) >= 0 && select32(w, k - before) < 32 && ((w >> select32(w, k - before)) & 1u));
-            classify_group_bf<FUSED>(P, xv0, y0 + j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
-                              S.b[j + 2], S.b[j + 3], S.bits, O);
+            classify_group_bf<FUSED>(P, xv0, j, select32(w, k - before), S.m[j], S.m[j + 1], S.m[j + 2], S.b[j + 1],
+                              S.b[j + 2], S.b[j + 3], D, O);
         }
     }
 }
