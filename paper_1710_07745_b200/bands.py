@@ -293,7 +293,11 @@ def _gather(tensor, world, group):
 def _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group):
     """Device pointers to the halo rows inside the neighbour bands (opened once
     per backend and band buffer over CUDA IPC: NVLink peer memory when the
-    neighbour is another GPU)."""
+    neighbour is another GPU), plus the step handshake: this rank's two
+    interprocess CUDA events ("band written", "halo rows read"), the
+    neighbours' events opened from their IPC handles, and a host-only (gloo)
+    group for the per-step barriers.  Set up collectively, once."""
+    import torch
     import torch.distributed as dist
 
     w = band_u8.shape[1]
@@ -302,26 +306,42 @@ def _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, g
         return be.peer_ptrs[1:]
     if getattr(be, "peer_ptrs", None) is not None:
         be.close_peers()
+    dev = band_u8.device
+    if getattr(be, "ev_written", None) is None:
+        with torch.cuda.device(dev):
+            be.ev_written = torch.cuda.Event(interprocess=True)  # my band is written (this step)
+            be.ev_read = torch.cuda.Event(interprocess=True)  # I have read my neighbours' rows (this step)
+            be.ev_written.record()  # materialised on this device before its handle is exported
+            be.ev_read.record()
+        # host-only barriers: a barrier of an NCCL group would wait for this rank's stream
+        be.host_group = group if dist.get_backend(group) == "gloo" else dist.new_group(
+            dist.get_process_group_ranks(group) if group is not None else None, backend="gloo")
     objs = [None] * world
-    dist.all_gather_object(objs, ipc_export(band_u8), group=group)
+    dist.all_gather_object(objs, (ipc_export(band_u8), bytes(be.ev_written.ipc_handle()),
+                                  bytes(be.ev_read.ipc_handle())), group=group)
     ht, hb = min(halo, row0), min(halo, full_height - row0 - rows)
     top = bot = 0
     be.peer_bases = []
+    be.peer_events = []  # (written, read) of every neighbour whose rows I read or who reads mine
     for peer, (p0, pr) in enumerate(meta):
         if peer == rank:
             continue
-        if ht and p0 + pr == row0:  # the band just above: its last ht rows
+        above, below = p0 + pr == row0, p0 == row0 + rows
+        if ht and above:  # the band just above: its last ht rows
             if pr < ht:
                 raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
-            ptr, base = ipc_open(*objs[peer])
+            ptr, base = ipc_open(*objs[peer][0])
             be.peer_bases.append(base)
             top = ptr + (pr - ht) * w
-        if hb and p0 == row0 + rows:  # the band just below: its first hb rows
+        if hb and below:  # the band just below: its first hb rows
             if pr < hb:
                 raise ValueError("peer halos need neighbour bands of at least radius+2 rows")
-            ptr, base = ipc_open(*objs[peer])
+            ptr, base = ipc_open(*objs[peer][0])
             be.peer_bases.append(base)
             bot = ptr
+        if above or below:
+            be.peer_events.append((torch.cuda.Event.from_ipc_handle(dev, objs[peer][1]),
+                                   torch.cuda.Event.from_ipc_handle(dev, objs[peer][2])))
     be.peer_ptrs = (key, top, ht, bot, hb)
     return be.peer_ptrs[1:]
 
@@ -339,9 +359,12 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     place from their HBM (CUDA IPC mappings of their band buffers, opened once;
     NVLink loads between GPUs).  Every rank's band must stay at the same address
     across calls and be written on the current stream before the call; the
-    call reads the neighbours' rows only after every band is written, and
-    returns only after every rank has finished reading, so the caller may
-    overwrite its band right away.
+    classifier reads the neighbours' rows only after every band's write (an
+    interprocess-event wait on the stream), and work the caller enqueues on
+    the stream after the call runs only after every neighbour has finished
+    reading, so the caller may enqueue its next write into its band right
+    away.  The host never waits for the GPU; it takes two host barriers per
+    call.
     Returns (labels, final) for those rows, equal to the rows of the
     whole-frame result."""
     import torch
@@ -368,18 +391,29 @@ def distributed_band_canny(band_u8, row0: int, full_height: int, weights, low: f
     hb = min(halo, full_height - row0 - rows)
     if peer:
         top, ht_, bot, hb_ = _peer_halos(be, band_u8, row0, rows, full_height, halo, meta, rank, world, group)
-        # two-phase host protocol: every band of this step is written before
-        # anyone reads its halo rows, and every rank has finished reading before
-        # any caller overwrites its band (the call returns only after both).
-        # (A device-side handshake -- cuStreamWaitValue32 on IPC-mapped flags --
-        # was measured: a stream waiting on a flag written by another context on
-        # the same GPU never resumed, so it is not used.)
+        # Two-phase handshake, ordered on the devices by interprocess CUDA
+        # events (no stream synchronisation: the host never waits for a GPU):
+        # (1) every rank records "band written" behind its write of this step;
+        # once every rank has ENQUEUED that record (host barrier), each stream
+        # waits on its neighbours' records before the classifier reads their
+        # rows; (2) likewise "halo rows read" after the classifier, which every
+        # stream waits on before its next work -- so a caller's next write into
+        # its band cannot overtake a neighbour still reading it.  The barrier
+        # is what makes a wait see THIS step's record (a wait issued before the
+        # record would see the previous one).  (A barrier-free handshake --
+        # cuStreamWaitValue32 on IPC-mapped flags -- was measured: a stream
+        # waiting on a flag written by another context on the same GPU never
+        # resumed, so it is not used.)
         stream = torch.cuda.current_stream(band_u8.device)
-        stream.synchronize()
-        dist.barrier(group=group)
+        be.ev_written.record(stream)
+        dist.barrier(group=be.host_group)
+        for written, _ in be.peer_events:
+            stream.wait_event(written)
         be.classify_trace_peer(band_u8, top, ht_, bot, hb_, row0, full_height, weights, low, high)
-        stream.synchronize()
-        dist.barrier(group=group)
+        be.ev_read.record(stream)
+        dist.barrier(group=be.host_group)
+        for _, read in be.peer_events:
+            stream.wait_event(read)
         return _merge_and_finalize(be, band_u8, rank, world, group)
     if staged is not None:
         if staged.shape != (ht + rows + hb, w) or staged[ht:ht + rows].data_ptr() != band_u8.data_ptr():

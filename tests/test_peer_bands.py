@@ -5,11 +5,16 @@ halo exchange step.
 The ranks are separate processes that share one GPU here (gpurun gives one
 B200): each maps its neighbours' band buffers over CUDA IPC exactly as it would
 map another GPU's (where the loads then travel over NVLink), and the group is
-gloo (NCCL refuses two ranks on one device).  No rank's kernel waits on another
-rank's kernel: every band is written before the group reads, and every rank
-has finished reading before any call returns.  The assembled result must
-equal the whole-frame call bit for bit, also when every rank writes a new
-frame into its band between calls (the write-after-read hazard).
+gloo (NCCL refuses two ranks on one device).  The steps are ordered on the
+device by interprocess CUDA events (bands.distributed_band_canny): a rank's
+stream waits for its neighbours' "band written" events before its classifier
+reads their rows, and for their "halo rows read" events before its next work;
+the host never synchronises a stream (no kernel spins on another's progress).
+The assembled result must equal the whole-frame call bit for bit, also when
+every rank enqueues a new frame into its band right after each call returns
+(the write-after-read hazard), and when one rank's stream runs far behind the
+others.  Negative control: with EF_TEST_PEER_NO_WAIT=1 (the event waits
+dropped) the delayed cases must fail (tools/gpu_peer.sh runs it).
 """
 
 import os
@@ -31,12 +36,14 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, frames, plan, weights, low, high, steps, out):
+def _worker(rank, world, port, frames, plan, weights, low, high, steps, out, delay_rank=-1):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
+    if os.environ.get("EF_TEST_PEER_NO_WAIT"):  # negative control only: drop the event waits (must then fail)
+        torch.cuda.Stream.wait_event = lambda self, event: None
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1710_07745_b200 import bands
@@ -48,6 +55,8 @@ def _worker(rank, world, port, frames, plan, weights, low, high, steps, out):
         be = bands.CudaBandBackend(e - s, w)
         res = []
         for step in range(steps):  # a new frame every call, written on this rank's stream
+            if rank == delay_rank:  # this rank's stream runs ~20 ms behind its neighbours' every step
+                torch.cuda._sleep(40_000_000)
             band.copy_(src[step % len(frames)])
             lab, fin = bands.distributed_band_canny(band, s, h, weights, low, high, backend=be, peer=True)
             res.append((lab.clone(), fin.clone()))  # stream-ordered snapshot, no host sync
@@ -59,8 +68,12 @@ def _worker(rank, world, port, frames, plan, weights, low, high, steps, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,radius", [(2, 2), (3, 2), (3, 5)])
-def test_peer_halo_bands_match_whole_frame(world, radius):
+@pytest.mark.parametrize("world,radius,delay_rank", [(2, 2, -1), (3, 2, -1), (3, 5, -1), (2, 2, 0), (2, 2, 1),
+                                                     (3, 2, 1)])
+def test_peer_halo_bands_match_whole_frame(world, radius, delay_rank):
+    """delay_rank: that rank's stream sleeps before each write, so without the
+    event ordering its neighbours would read its rows before they are written
+    (delay 0) or write their next frame while it still reads theirs (delay 1)."""
     import torch.multiprocessing as mp
 
     from paper_1710_07745_b200 import bands, canny, synth
@@ -76,7 +89,8 @@ def test_peer_halo_bands_match_whole_frame(world, radius):
     manager = mp.Manager()
     out = manager.dict()
     steps = 5
-    mp.spawn(_worker, args=(world, _free_port(), frames, plan, w, 20.0, 50.0, steps, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), frames, plan, w, 20.0, 50.0, steps, out, delay_rank), nprocs=world,
+             join=True)
     for rank, (s, e) in enumerate(plan):
         for step in range(steps):
             bl, bf = out[rank][step]
