@@ -155,7 +155,10 @@ int ef_laplacian_f64(const double* d_src, int32_t height, int32_t width, double*
 /* Host-buffer entry point (the e2e path a drop-in user calls): copies u8 frames
  * from h_src to the device, runs ef_canny_u8, and copies labels/final back,
  * overlapping copies and compute across frame chunks on internal streams.
- * Pinned host buffers give full PCIe bandwidth.  Synchronous on return. */
+ * Pinned host buffers give full PCIe bandwidth.  Synchronous on return.
+ * h_labels may be NULL (edges only -- what the CLI's detect path and
+ * edges_to_image, bench.py:129-133, consume): the edge map then crosses PCIe
+ * at 1 bit per pixel instead of 2 and only h_final is written. */
 int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_t width,
                      const double* h_weights, int32_t radius, double low, double high,
                      uint8_t* h_labels, uint8_t* h_final, int32_t device);

@@ -260,10 +260,12 @@ def laplacian_f64(frame, stream=None):
 
 
 def canny_u8_host(frames: np.ndarray, weights, low: float, high: float, labels: np.ndarray | None = None,
-                  final: np.ndarray | None = None, device: int | None = None):
+                  final: np.ndarray | None = None, device: int | None = None, edges_only: bool = False):
     """Host buffers in, host buffers out: the e2e entry point (H2D + kernels + D2H
     pipelined inside the library).  Pinned (page-locked) buffers give full
-    PCIe bandwidth; pageable ones work but are staged."""
+    PCIe bandwidth; pageable ones work but are staged.  edges_only=True returns
+    (None, final): the labels stay on the device and the edge map comes back at
+    1 bit per pixel."""
     torch = require_cuda()
     arr = np.asarray(frames)
     if arr.dtype != np.uint8:
@@ -271,27 +273,32 @@ def canny_u8_host(frames: np.ndarray, weights, low: float, high: float, labels: 
     squeeze = arr.ndim == 2
     x = np.ascontiguousarray(arr[None] if squeeze else arr)
     b, h, w = x.shape
-    labels = np.empty(x.shape, np.uint8) if labels is None else labels
+    if edges_only and labels is not None:
+        raise ValueError("edges_only=True takes no labels array")
+    labels = None if edges_only else (np.empty(x.shape, np.uint8) if labels is None else labels)
     final = np.empty(x.shape, np.uint8) if final is None else final
     for name, a in (("labels", labels), ("final", final)):
+        if a is None:
+            continue
         if (a.shape != x.shape or a.dtype != np.uint8 or not a.flags.c_contiguous or not a.flags.writeable):
             raise ValueError(f"{name} must be a writeable C-contiguous uint8 array of shape {x.shape}")
     _, wp, r = host_weights(weights)
     dev = torch.cuda.current_device() if device is None else int(device)
     rc = _lib.load().ef_canny_u8_host(x.ctypes.data, b, h, w, wp, r, float(low), float(high),
-                                      labels.ctypes.data, final.ctypes.data, dev)
+                                      None if labels is None else labels.ctypes.data, final.ctypes.data, dev)
     _lib.check(rc, "ef_canny_u8_host")
     if squeeze:
-        return labels[0], final[0]
+        return (None if labels is None else labels[0]), final[0]
     return labels, final
 
 
 def canny_u8_host_ptr(src_ptr: int, batch: int, height: int, width: int, weights, low: float, high: float,
                       labels_ptr: int, final_ptr: int, device: int = 0) -> None:
-    """Raw-pointer form of canny_u8_host (pinned torch CPU tensors in bench.py)."""
+    """Raw-pointer form of canny_u8_host (pinned torch CPU tensors in bench.py);
+    labels_ptr 0 / None = edges only."""
     _, wp, r = host_weights(weights)
     rc = _lib.load().ef_canny_u8_host(src_ptr, batch, height, width, wp, r, float(low), float(high),
-                                      labels_ptr, final_ptr, device)
+                                      labels_ptr or None, final_ptr, device)
     _lib.check(rc, "ef_canny_u8_host")
 
 

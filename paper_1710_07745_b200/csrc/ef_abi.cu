@@ -650,7 +650,8 @@ HostCtx& host_ctx(int dev) {
 }
 
 void unpack_part(PackSlot* s, size_t b0, size_t b1) {
-    unpack_codes(s->packed, b0, b1, s->npx, s->labels, s->final_map);
+    if (s->labels) unpack_codes(s->packed, b0, b1, s->npx, s->labels, s->final_map);
+    else unpack_bits(s->packed, b0, b1, s->npx, s->final_map);  // edges-only call
     flush_lines(s->packed + b0, b1 - b0);
 }
 
@@ -750,7 +751,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
                      int32_t device) {
     int rc;
     if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
-    if (!h_src || !h_labels || !h_final) return fail(EF_EINVAL, "NULL buffer");
+    if (!h_src || !h_final) return fail(EF_EINVAL, "NULL buffer");  // h_labels == NULL: edges only
     EF_CHECK(cudaSetDevice(device), "cudaSetDevice");
     HostCtx& C = host_ctx(device);
     std::lock_guard<std::mutex> lk(C.mu);
@@ -844,13 +845,14 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
             drain(C);
             return rc;
         }
-        const size_t pbytes = (bytes + 3) / 4;
-        e = launch_pack(d_lab, d_fin, (long long)bytes, d_packed, sms, st);
+        const size_t pbytes = h_labels ? (bytes + 3) / 4 : (bytes + 7) / 8;
+        e = h_labels ? launch_pack(d_lab, d_fin, (long long)bytes, d_packed, sms, st)
+                     : launch_pack_final(d_fin, (long long)bytes, d_packed, sms, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(s.packed, d_packed, pbytes, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) {
             s.nbytes = pbytes;
             s.npx = bytes;
-            s.labels = h_labels + f0 * fpx;
+            s.labels = h_labels ? h_labels + f0 * fpx : nullptr;
             s.final_map = h_final + f0 * fpx;
             s.last = i + 1 == plan.size();
             e = cudaEventRecord(s.done, st);

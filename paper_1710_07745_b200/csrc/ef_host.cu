@@ -77,6 +77,40 @@ cudaError_t launch_pack(const uint8_t* labels, const uint8_t* final_map, long lo
     return cudaGetLastError();
 }
 
+// Edges-only calls (h_labels == NULL): the final map alone, 1 bit per pixel
+// (bit k of byte j = pixel 8 j + k).  32 pixels -> 4 packed bytes per thread.
+__global__ void pack_final_kernel(const uint8_t* __restrict__ final_map, long long n, uint8_t* __restrict__ packed) {
+    const long long nq = (n + 31) / 32;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+        const long long p0 = q * 32;
+        uint32_t out = 0;
+        if (p0 + 32 <= n) {
+            const uint4 a = *reinterpret_cast<const uint4*>(final_map + p0);
+            const uint4 b = *reinterpret_cast<const uint4*>(final_map + p0 + 16);
+            const uint32_t fw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k)  // bytes are 0 / 1: gather the four low bits of a word into a nibble
+                out |= (((fw[k] & 0x01010101u) * 0x10204080u) >> 28) << (4 * k);
+        } else {
+            for (int k = 0; p0 + k < n; ++k) out |= (uint32_t)(final_map[p0 + k] & 1u) << k;
+        }
+        const long long nb = min(4ll, (n - p0 + 7) / 8);  // packed bytes this thread owns
+        if (nb == 4) *reinterpret_cast<uint32_t*>(packed + 4 * q) = out;
+        else
+            for (int b = 0; b < nb; ++b) packed[4 * q + b] = (uint8_t)(out >> (8 * b));
+    }
+}
+
+cudaError_t launch_pack_final(const uint8_t* final_map, long long n, uint8_t* packed, int sm_count, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const long long nq = (n + 31) / 32;
+    const int threads = 256;
+    const long long want = (nq + threads - 1) / threads;
+    const int blocks = (int)std::min<long long>(want, (long long)sm_count * 8);
+    pack_final_kernel<<<blocks, threads, 0, st>>>(final_map, n, packed);
+    return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------- host ----
 namespace {
 struct Luts {
@@ -195,6 +229,43 @@ void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx,
             final_map[4 * j + k] = (uint8_t)(f >> (8 * k));
         }
     }
+}
+
+#if EF_X86
+// 4 packed bytes (32 pixels) per step: pdep spreads 8 bits into 8 bytes of 0 / 1.
+__attribute__((target("avx2,bmi2"))) static size_t unpack_bits_avx2(const uint8_t* packed, size_t j, size_t end,
+                                                                     uint8_t* final_map) {
+    const uint64_t ones = 0x0101010101010101ull;
+    for (; j + 4 <= end; j += 4) {
+        uint32_t w;
+        std::memcpy(&w, packed + j, 4);
+        const __m256i v = _mm256_setr_epi64x((long long)_pdep_u64(w & 0xffu, ones), (long long)_pdep_u64((w >> 8) & 0xffu, ones),
+                                             (long long)_pdep_u64((w >> 16) & 0xffu, ones), (long long)_pdep_u64(w >> 24, ones));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(final_map + 8 * j), v);
+    }
+    return j;
+}
+#endif
+
+// expand packed bits [byte0, byte1) of an npx-pixel stream into final_map (0 / 1 bytes)
+void unpack_bits(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx, uint8_t* final_map) {
+    auto scalar = [&](size_t b) {
+        uint64_t v = 0;
+        for (int k = 0; k < 8; ++k) v |= (uint64_t)((packed[b] >> k) & 1u) << (8 * k);
+        std::memcpy(final_map + 8 * b, &v, 8);
+    };
+    size_t j = byte0;
+    const size_t full_end = std::min(byte1, npx / 8);  // bytes whose 8 pixels all exist
+#if EF_X86
+    if (has_avx2_bmi2()) {
+        while (j < full_end && (reinterpret_cast<uintptr_t>(final_map + 8 * j) & 31)) scalar(j++);
+        if ((reinterpret_cast<uintptr_t>(final_map + 8 * j) & 31) == 0) j = unpack_bits_avx2(packed, j, full_end, final_map);
+        _mm_sfence();
+    }
+#endif
+    for (; j < full_end; ++j) scalar(j);
+    if (j < byte1 && 8 * j < npx)  // last partial byte
+        for (size_t k = 0; 8 * j + k < npx; ++k) final_map[8 * j + k] = (uint8_t)((packed[j] >> k) & 1u);
 }
 
 // Fixed pool of worker threads with a FIFO (front pushes jump the queue).

@@ -19,6 +19,10 @@ cudaError_t launch_pack(const uint8_t* labels, const uint8_t* final_map, long lo
 void unpack_codes(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx, uint8_t* labels,
                   uint8_t* final_map);
 
+// edges-only calls: the final map alone at 1 bit per pixel (bit k of byte j = pixel 8 j + k)
+cudaError_t launch_pack_final(const uint8_t* final_map, long long n, uint8_t* packed, int sm_count, cudaStream_t st);
+void unpack_bits(const uint8_t* packed, size_t byte0, size_t byte1, size_t npx, uint8_t* final_map);
+
 void flush_lines(const uint8_t* p, size_t n);
 
 class HostPool {

@@ -487,6 +487,27 @@ def test_host_entry_pinned_pageable_and_misaligned_outputs(canny):
     assert np.array_equal(hl, lab) and np.array_equal(hf, fin)
 
 
+@pytest.mark.parametrize("shape", [(5, 67, 131), (7, 33, 64), (1, 1, 3), (1, 1, 9), (9, 120, 160), (3, 256, 256)])
+def test_host_entry_edges_only(canny, shape):
+    """h_labels == NULL: the edge map alone crosses PCIe at 1 bit/px; the bytes
+    written equal the oracle's final map (odd pixel counts, chunk tails, outputs at
+    odd addresses with guard bytes around them)."""
+    rng = np.random.default_rng(sum(shape) + 1)
+    frames = synth.config3(shape[0], 256)[:, :shape[1], :shape[2]].copy() if shape[1] > 8 else \
+        rng.integers(0, 256, size=shape, dtype=np.uint8)
+    w = O.gaussian_weights(1.4, radius=2)
+    _, want = O.canny(frames, w, 20.0, 50.0)
+    none, hf = canny.canny_u8_host(frames, w, 20.0, 50.0, edges_only=True)
+    assert none is None and np.array_equal(hf.astype(bool), want)
+    assert set(np.unique(hf)) <= {0, 1}
+    for phase in (1, 8, 32):
+        big = np.full(frames.size + 96, 7, np.uint8)
+        out = big[phase:phase + frames.size].reshape(frames.shape)
+        canny.canny_u8_host_ptr(frames.ctypes.data, *frames.shape, w, 20.0, 50.0, 0, out.ctypes.data)
+        assert np.array_equal(out.astype(bool), want)
+        assert (big[:phase] == 7).all() and (big[phase + frames.size:] == 7).all()
+
+
 def test_invalid_arguments_raise_valueerror(canny):
     w = O.gaussian_weights(1.4)
     img = _dev(np.zeros((8, 8), np.uint8))
