@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose and (res.stdout or res.stderr):
                 print(res.stdout, res.stderr, file=sys.stderr)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

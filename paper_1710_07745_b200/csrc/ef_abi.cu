@@ -5,6 +5,7 @@
 // fast path, workspace layout, kernel sequencing, the host-buffer pipeline and
 // the cross-band union-find.
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost a function-pointer check when no tool is attached
 
 #include <algorithm>
 #include <atomic>
@@ -26,6 +27,15 @@ using namespace ef;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over a host-side section (kernel enqueue sequences, host-buffer chunks):
+// shows the library's phases in Nsight Systems timelines
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+    Range(const Range&) = delete;
+    Range& operator=(const Range&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -316,6 +326,7 @@ bool has_negative(const double* w, int r) {
 int run_classify_u8(const uint8_t* src, int64_t batch, const FrameGeom& g, const double* w, int r,
                     double low, double high, uint8_t* labels, const Ws& ws, const WsLayout& L,
                     cudaStream_t st, uint8_t* fin = nullptr, FgBits* bits = nullptr) {
+    Range nvtx("edgeforge classify (ws_begin, K1, fix-ups)");
     int sms = sm_count_current();
     if (bits) *bits = FgBits{};
     if (has_negative(w, r)) {
@@ -366,6 +377,7 @@ FgBits ws_planes(const Ws& ws, int H, int W) {
 // classify launch of this call (standalone tracing).
 int run_trace(const uint8_t* labels, int64_t batch, int H, int W, uint8_t* fin, const Ws& ws, const WsLayout& L,
               cudaStream_t st, bool finalize, bool reset, const FgBits* bits = nullptr) {
+    Range nvtx("edgeforge trace (H1-H4)");
     const int sms = sm_count_current();
     if (reset) EF_CHECK(launch_ws_begin(ws, L, 0, sms, st), "ws_begin");
     FgBits B;
@@ -650,6 +662,7 @@ HostCtx& host_ctx(int dev) {
 }
 
 void unpack_part(PackSlot* s, size_t b0, size_t b1) {
+    Range nvtx("edgeforge host unpack");
     if (s->labels) unpack_codes(s->packed, b0, b1, s->npx, s->labels, s->final_map);
     else unpack_bits(s->packed, b0, b1, s->npx, s->final_map);  // edges-only call
     flush_lines(s->packed + b0, b1 - b0);
@@ -752,6 +765,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
     int rc;
     if ((rc = check_dims(batch, height, width)) || (rc = check_params(h_weights, radius, low, high))) return rc;
     if (!h_src || !h_final) return fail(EF_EINVAL, "NULL buffer");  // h_labels == NULL: edges only
+    Range nvtx("edgeforge canny_u8_host");
     EF_CHECK(cudaSetDevice(device), "cudaSetDevice");
     HostCtx& C = host_ctx(device);
     std::lock_guard<std::mutex> lk(C.mu);
@@ -809,6 +823,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
     const int sms = sm_count_current();
     int64_t f0 = 0;
     for (size_t i = 0; i < plan.size(); f0 += plan[i], ++i) {
+        Range nvtx_chunk("edgeforge host chunk (H2D, kernels, packed D2H)");
         const int k = (int)(i % kHostStreams);
         PackSlot& s = C.slot[i % kPackSlots];
         const int64_t n = plan[i];
