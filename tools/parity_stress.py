@@ -56,6 +56,21 @@ def main():
                                            "low": low, "high": high}}))
             sys.exit(1)
     print(json.dumps({"group": "random", "images": n, "pixels": checked, "seed": seed, "mismatches": 0}))
+    # host-buffer entry on random batches: labels + final, and edges only (1 bit/px transfer)
+    hb = 0
+    for i in range(max(1, n // 10)):
+        b, h, w = int(rng.integers(1, 9)), int(rng.integers(1, 300)), int(rng.integers(1, 400))
+        frames = rng.integers(0, 256, (b, h, w), dtype=np.uint8)
+        wts = O.gaussian_weights(1.4, radius=int(rng.integers(1, 4)))
+        el, ef = O.canny(frames, wts, 20.0, 50.0)
+        hl, hf = canny.canny_u8_host(frames, wts, 20.0, 50.0)
+        _, of = canny.canny_u8_host(frames, wts, 20.0, 50.0, edges_only=True)
+        if not (np.array_equal(hl, el) and np.array_equal(hf.astype(bool), ef) and np.array_equal(of, hf)):
+            print(json.dumps({"mismatch": {"host_batch": [b, h, w], "i": i}}))
+            sys.exit(1)
+        hb += frames.size
+    print(json.dumps({"group": "host-buffer entry (labels+final, edges only)", "batches": max(1, n // 10),
+                      "pixels": hb, "mismatches": 0}))
     # full C1 (64 x 1080p) at the reference's default kernel (radius 5)
     frames = synth.config_range(1, 0, 64)
     wts = O.gaussian_weights(1.4)
