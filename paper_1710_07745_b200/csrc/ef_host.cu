@@ -357,9 +357,38 @@ static void stream_copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
 #endif
 }
 
+#if EF_X86
+// 8 doubles per step: truncate, convert back and compare (NaN and out-of-range
+// values fail the comparison or the range test), pack to bytes with saturation
+// (dst is unspecified once a value failed).  Returns the first index not done.
+__attribute__((target("avx2"))) static size_t f64_to_u8_avx2(const double* src, size_t n, uint8_t* dst, bool& ok) {
+    __m256d bad = _mm256_setzero_pd();
+    const __m128i lim = _mm_set1_epi32(255);
+    __m128i badi = _mm_setzero_si128();
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        const __m256d a = _mm256_loadu_pd(src + i), b = _mm256_loadu_pd(src + i + 4);
+        const __m128i ta = _mm256_cvttpd_epi32(a), tb = _mm256_cvttpd_epi32(b);
+        bad = _mm256_or_pd(bad, _mm256_cmp_pd(_mm256_cvtepi32_pd(ta), a, _CMP_NEQ_UQ));
+        bad = _mm256_or_pd(bad, _mm256_cmp_pd(_mm256_cvtepi32_pd(tb), b, _CMP_NEQ_UQ));
+        // 0 <= t <= 255 as one unsigned comparison per lane (max_epu32(t, 255) == 255)
+        badi = _mm_or_si128(badi, _mm_xor_si128(_mm_max_epu32(ta, lim), lim));
+        badi = _mm_or_si128(badi, _mm_xor_si128(_mm_max_epu32(tb, lim), lim));
+        const __m128i w16 = _mm_packus_epi32(ta, tb);
+        _mm_storel_epi64(reinterpret_cast<__m128i*>(dst + i), _mm_packus_epi16(w16, w16));
+    }
+    ok = _mm256_movemask_pd(bad) == 0 && _mm_testz_si128(badi, badi);
+    return i;
+}
+#endif
+
 static bool f64_to_u8(const double* src, size_t n, uint8_t* dst) {
     bool ok = true;
-    for (size_t i = 0; i < n; ++i) {
+    size_t i0 = 0;
+#if EF_X86
+    if (has_avx2_bmi2()) i0 = f64_to_u8_avx2(src, n, dst, ok);
+#endif
+    for (size_t i = i0; i < n; ++i) {
         const double v = src[i];
         const bool in = v >= 0.0 && v <= 255.0;  // false for NaN
         const int t = in ? (int)v : 0;

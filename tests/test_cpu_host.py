@@ -192,6 +192,38 @@ def test_host_f64_to_u8_integer_test():
     assert ef.GrayImage.from_array(np.zeros((3, 5))).as_u8() is not None
 
 
+def test_host_f64_to_u8_vector_body_and_tail():
+    """ef_host_f64_to_u8 directly: the 8-wide vector body and the scalar tail agree
+    with numpy for every length 0..40 and for a bad value at every position --
+    NaN, +-inf, -0.0 (an integer: accepted), 2^31, 2^53, denormals, 255 + 1ulp."""
+    lib = _lib.load()
+    rng = np.random.default_rng(9)
+
+    def call(a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.full(a.size + 8, 0xAB, np.uint8)
+        rc = lib.ef_host_f64_to_u8(a.ctypes.data, a.size, out.ctypes.data)
+        assert (out[a.size:] == 0xAB).all()
+        return rc, out[:a.size]
+
+    for n in range(0, 41):
+        a = rng.integers(0, 256, n).astype(np.float64)
+        rc, out = call(a)
+        assert rc == 1 and np.array_equal(out, a.astype(np.uint8)), n
+    base = rng.integers(0, 256, 37).astype(np.float64)
+    bads = [np.nan, np.inf, -np.inf, 2.0 ** 31, -2.0 ** 31, 2.0 ** 53, 5e-324, -5e-324, np.nextafter(255.0, 256.0),
+            np.nextafter(0.0, -1.0), 0.5, -1.0, 256.0, 1e300]
+    for pos in range(37):
+        for bad in bads:
+            b = base.copy()
+            b[pos] = bad
+            assert call(b)[0] == 0, (pos, bad)
+        b = base.copy()
+        b[pos] = -0.0
+        rc, out = call(b)
+        assert rc == 1 and out[pos] == 0
+
+
 def _canny_u8_call(weights, ws_ptr=None, ws_bytes=1 << 30):
     """ef_canny_u8 with dummy device pointers: argument validation runs on the
     host before anything touches a device, so the status and message are
