@@ -11,9 +11,11 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -673,9 +675,29 @@ void unpack_part(PackSlot* s, size_t b0, size_t b1) {
 // the stream -- and the next chunk's H2D behind it -- until it returns.)
 void fan_out_unpack(PackSlot* s);
 
+#ifndef EF_HOST_POLL
+#define EF_HOST_POLL 1
+#endif
+
+// Wait for a chunk's event without holding a core and without depending on an
+// interrupt: poll with short sleeps.  (Blocking-sync events slept through a lost
+// wake-up about once in 25 one-GiB calls on the measured host: one call of 80 ms
+// among 24 ms ones, always ~56 ms late.)
+cudaError_t wait_event(cudaEvent_t ev) {
+#if EF_HOST_POLL
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(ev);
+        if (q != cudaErrorNotReady) return q;
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+#else
+    return cudaEventSynchronize(ev);
+#endif
+}
+
 void wait_and_unpack(PackSlot* s, int device) {
     cudaSetDevice(device);
-    if (cudaEventSynchronize(s->done) != cudaSuccess) {
+    if (wait_event(s->done) != cudaSuccess) {
         s->failed = true;
         s->latch.done();
         return;
@@ -786,14 +808,14 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
     const int src_kind = host_kind(h_src, (size_t)batch * fpx);
     if (C.dev != device) {
         C.dev = device;
-        // blocking-sync events: a pool thread waiting on a chunk sleeps instead
-        // of spinning on a core the unpack needs
+        // a pool thread waiting on a chunk must not spin on a core the unpack needs:
+        // wait_event polls with short sleeps (EF_HOST_POLL=0: blocking-sync events)
+        const unsigned evflags = cudaEventDisableTiming | (EF_HOST_POLL ? 0u : (unsigned)cudaEventBlockingSync);
         for (int i = 0; i < kHostStreams; ++i) {
             EF_CHECK(cudaStreamCreateWithFlags(&C.st[i], cudaStreamNonBlocking), "stream");
-            EF_CHECK(cudaEventCreateWithFlags(&C.h2d[i], cudaEventDisableTiming | cudaEventBlockingSync), "event");
+            EF_CHECK(cudaEventCreateWithFlags(&C.h2d[i], evflags), "event");
         }
-        for (auto& s : C.slot)
-            EF_CHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+        for (auto& s : C.slot) EF_CHECK(cudaEventCreateWithFlags(&s.done, evflags), "event");
     }
     if (C.buf_px < need_px || C.ws_bytes < need_ws) {
         for (int i = 0; i < kHostStreams; ++i) {
@@ -849,7 +871,7 @@ int ef_canny_u8_host(const uint8_t* h_src, int64_t batch, int32_t height, int32_
         }
         const uint8_t* src = h_src + f0 * fpx;
         if (e == cudaSuccess && src_kind == 1) {
-            if (C.h2d_pending[k]) e = cudaEventSynchronize(C.h2d[k]);
+            if (C.h2d_pending[k]) e = wait_event(C.h2d[k]);
             if (e == cudaSuccess) parallel_copy(C.stage[k], src, bytes);
             src = C.stage[k];
         }
