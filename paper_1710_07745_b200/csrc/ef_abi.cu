@@ -678,6 +678,9 @@ void fan_out_unpack(PackSlot* s);
 #ifndef EF_HOST_POLL
 #define EF_HOST_POLL 1
 #endif
+#ifndef EF_HOST_POLL_US
+#define EF_HOST_POLL_US 20
+#endif
 
 // Wait for a chunk's event without holding a core and without depending on an
 // interrupt: poll with short sleeps.  (Blocking-sync events slept through a lost
@@ -688,7 +691,7 @@ cudaError_t wait_event(cudaEvent_t ev) {
     for (;;) {
         const cudaError_t q = cudaEventQuery(ev);
         if (q != cudaErrorNotReady) return q;
-        std::this_thread::sleep_for(std::chrono::microseconds(20));
+        std::this_thread::sleep_for(std::chrono::microseconds(EF_HOST_POLL_US));
     }
 #else
     return cudaEventSynchronize(ev);
