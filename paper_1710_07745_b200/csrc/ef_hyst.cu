@@ -430,13 +430,18 @@ __device__ __forceinline__ void tile_ccl(const TileGeo& g, TileCCL& s, uint32_t 
 __device__ __forceinline__ void warp_rows(const FgBits& B, const TileGeo& g, int lane, int H, unsigned long long& f0,
                                           unsigned long long& f1, unsigned long long& s0, unsigned long long& s1) {
     const int ya = g.y0 + 2 * lane;
-    const unsigned long long t0 = plane_word(B.st, B, g.f, ya, H, g.txi);
-    const unsigned long long t1 = plane_word(B.st, B, g.f, ya + 1, H, g.txi);
-    f0 = plane_word(B.fg, B, g.f, ya, H, g.txi) & ~t0;
-    f1 = plane_word(B.fg, B, g.f, ya + 1, H, g.txi) & ~t1;
+    // the tile's word column exists (txi < words) and ya >= 0: one 64-bit word index for
+    // the lane's four loads, row checks only against the frame's last row
+    const unsigned long long w0 =
+        (unsigned long long)g.f * B.frame_words + (unsigned long long)ya * (unsigned)B.words + (unsigned)g.txi;
+    const bool in0 = ya < H, in1 = ya + 1 < H;
+    const unsigned long long t0 = in0 ? __ldg(B.st + w0) : 0ull;
+    const unsigned long long t1 = in1 ? __ldg(B.st + w0 + B.words) : 0ull;
+    f0 = (in0 ? __ldg(B.fg + w0) : 0ull) & ~t0;
+    f1 = (in1 ? __ldg(B.fg + w0 + B.words) : 0ull) & ~t1;
     unsigned long long up = __shfl_up_sync(0xffffffffu, t1, 1), dn = __shfl_down_sync(0xffffffffu, t0, 1);
-    if (lane == 0) up = plane_word(B.st, B, g.f, g.y0 - 1, H, g.txi);
-    if (lane == 31) dn = plane_word(B.st, B, g.f, g.y0 + HT, H, g.txi);
+    if (lane == 0) up = g.y0 > 0 ? __ldg(B.st + w0 - B.words) : 0ull;
+    if (lane == 31) dn = g.y0 + HT < H ? __ldg(B.st + w0 + 2 * (unsigned long long)B.words) : 0ull;
     const unsigned long long v0 = up | t0 | t1, v1 = t0 | t1 | dn;
     s0 = f0 ? f0 & (v0 | (v0 << 1) | (v0 >> 1) | side_strong(B, g.f, ya, H, g.txi, f0)) : 0ull;
     s1 = f1 ? f1 & (v1 | (v1 << 1) | (v1 >> 1) | side_strong(B, g.f, ya + 1, H, g.txi, f1)) : 0ull;
