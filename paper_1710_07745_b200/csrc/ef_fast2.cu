@@ -67,6 +67,9 @@ constexpr int V2_COLS = 128;
 #ifndef EF_K1_HODD
 #define EF_K1_HODD 1  // odd horizontal taps as one FFMA2 over two scalar sums (0: four scalar ops)
 #endif
+#ifndef EF_K1_EDGEPRED
+#define EF_K1_EDGEPRED 1  // classifier: a group's edge columns are loaded only for edge pixels that can be foreground
+#endif
 #ifndef EF_K1_MINB
 #define EF_K1_MINB 6  // CTAs per SM the register budget is sized for (shared memory allows 6 at TH = 32)
 #endif
@@ -220,6 +223,7 @@ __device__ __forceinline__ void v2_phase1(int xv0, int y0, const FastParams& P, 
 // The few scalars the classifier needs (kept in registers).
 struct V2Cls {
     float lo_lo, lo_hi, hi_lo, hi_hi, e_nms0, e_nms_rel, e_sec;
+    float cand_sq;  // squared magnitudes below this are certainly below `low` (phase 2's candidate test)
     int cls0;
     int W, FH, out0;
 };
@@ -237,6 +241,19 @@ __device__ __forceinline__ void load6(const float* row, int cc0, float (&v)[6]) 
     v[0] = row[cc0 - 1];
     v[1] = mid.x; v[2] = mid.y; v[3] = mid.z; v[4] = mid.w;
     v[5] = row[cc0 + 4];
+}
+
+// The column left of the group is read only by its pixel 0 and the column right of it
+// only by pixel 3 (neighbours and Sobel taps of those pixels).  A pixel certainly below
+// `low` gets the background class whatever its neighbours are, so its edge column is
+// not loaded: the scalar edge loads are 4-way bank-conflicted by construction
+// (elements 3 / 0 of a quad live in 8 of the 32 banks) and a third of the groups' edge
+// pixels are below `low` -- fewer lanes per load, fewer wavefronts on the LSU pipe.
+__device__ __forceinline__ void load6_edges(const float* row, int cc0, bool left, bool right, float (&v)[6]) {
+    const float4 mid = *reinterpret_cast<const float4*>(row + cc0);
+    v[0] = left ? row[cc0 - 1] : 0.f;
+    v[1] = mid.x; v[2] = mid.y; v[3] = mid.z; v[4] = mid.w;
+    v[5] = right ? row[cc0 + 4] : 0.f;
 }
 
 // The tile's output addresses, formed once per thread before the classifier's
@@ -260,12 +277,27 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int j
     const float t1 = 0.41421356237309503f;
     const int cc0 = 4 * cl;
     float Mu[6], Mc[6], Md[6], Bu[6], Bm[6], Bd[6];
+#if EF_K1_EDGEPRED
+    {
+        const float4 mid = *reinterpret_cast<const float4*>(mc + cc0);
+        Mc[1] = mid.x; Mc[2] = mid.y; Mc[3] = mid.z; Mc[4] = mid.w;
+        const bool left = Mc[1] >= P.cand_sq, right = Mc[4] >= P.cand_sq;
+        Mc[0] = left ? mc[cc0 - 1] : 0.f;
+        Mc[5] = right ? mc[cc0 + 4] : 0.f;
+        load6_edges(mu, cc0, left, right, Mu);
+        load6_edges(md, cc0, left, right, Md);
+        load6_edges(bu, cc0, left, right, Bu);
+        load6_edges(bm, cc0, left, right, Bm);
+        load6_edges(bd, cc0, left, right, Bd);
+    }
+#else
     load6(mu, cc0, Mu);
     load6(mc, cc0, Mc);
     load6(md, cc0, Md);
     load6(bu, cc0, Bu);
     load6(bm, cc0, Bm);
     load6(bd, cc0, Bd);
+#endif
     uint32_t packed = 0;
     bool any_flag = false;
     const uint32_t cls0 = (uint32_t)P.cls0;
@@ -730,7 +762,9 @@ k1v3_kernel(const uint8_t* __restrict__ src, FrameGeom g, FastParams P, uint8_t*
     if (!interior)  // magnitudes: row j <-> frame row y0-1+j
         replicate_edges<V3_MROWS, V2_COLS, V2_CS>(S.m, max(0, -xv0), min(V2_COLS - 1, W - 1 - xv0),
                                                   max(0, -(y0 - 1)), min(V3_MROWS - 1, FH - 1 - (y0 - 1)), 1);
-    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec, P.cls0, g.W, g.full_H, g.out0};
+    const V2Cls CP{P.lo_lo, P.lo_hi, P.hi_lo, P.hi_hi, P.e_nms0, P.e_nms_rel, P.e_sec,
+                   P.lo_lo > 0.f ? P.lo_lo * P.lo_lo * (1.0f - 1.0f / 262144.0f) : -1.0f,  // as phase 2's cand_sq
+                   P.cls0, g.W, g.full_H, g.out0};
     v3_classify<R, FUSED>(CP, xv0, y0, S, warp, lane, O);
 }
 
