@@ -68,7 +68,8 @@ constexpr int V2_COLS = 128;
 #define EF_K1_HODD 1  // odd horizontal taps as one FFMA2 over two scalar sums (0: four scalar ops)
 #endif
 #ifndef EF_K1_EDGEPRED
-#define EF_K1_EDGEPRED 1  // classifier: a group's edge columns are loaded only for edge pixels that can be foreground
+#define EF_K1_EDGEPRED 2  // classifier: a group's edge columns are loaded only for edge pixels that can be
+                          // foreground (1), the magnitude tile's only in the row the pixel's sector picks (2)
 #endif
 #ifndef EF_K1_MINB
 #define EF_K1_MINB 6  // CTAs per SM the register budget is sized for (shared memory allows 6 at TH = 32)
@@ -277,15 +278,27 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int j
     const float t1 = 0.41421356237309503f;
     const int cc0 = 4 * cl;
     float Mu[6], Mc[6], Md[6], Bu[6], Bm[6], Bd[6];
+    bool left = true, right = true;  // the group's pixel 0 / 3 can be foreground
+    (void)left;
+    (void)right;
 #if EF_K1_EDGEPRED
     {
         const float4 mid = *reinterpret_cast<const float4*>(mc + cc0);
         Mc[1] = mid.x; Mc[2] = mid.y; Mc[3] = mid.z; Mc[4] = mid.w;
-        const bool left = Mc[1] >= P.cand_sq, right = Mc[4] >= P.cand_sq;
+        left = Mc[1] >= P.cand_sq;
+        right = Mc[4] >= P.cand_sq;
+#if EF_K1_EDGEPRED >= 2
+        // the magnitude tile's edge columns: one value per edge pixel, loaded once its
+        // sector is known (below); only the blurred tile's edges are needed up front
+        Mc[0] = Mc[5] = 0.f;
+        load6_edges(mu, cc0, false, false, Mu);
+        load6_edges(md, cc0, false, false, Md);
+#else
         Mc[0] = left ? mc[cc0 - 1] : 0.f;
         Mc[5] = right ? mc[cc0 + 4] : 0.f;
         load6_edges(mu, cc0, left, right, Mu);
         load6_edges(md, cc0, left, right, Md);
+#endif
         load6_edges(bu, cc0, left, right, Bu);
         load6_edges(bm, cc0, left, right, Bm);
         load6_edges(bd, cc0, left, right, Bd);
@@ -314,7 +327,20 @@ __device__ __forceinline__ void classify_group_bf(const V2Cls& P, int xv0, int j
         const float n45 = fmaxf(Mu[k + 2], Md[k]);
         const float n135 = fmaxf(Mu[k], Md[k + 2]);
         const float ndiag = ((gx > 0.f) == (gy > 0.f)) ? n45 : n135;
-        const float nmax = uu > 0.f ? n0 : (vv > 0.f ? n90 : ndiag);
+        float nmax = uu > 0.f ? n0 : (vv > 0.f ? n90 : ndiag);
+#if EF_K1_EDGEPRED >= 2
+        if (k == 0 || k == 3) {
+            // the edge pixel's neighbour in the column outside the group sits in the row
+            // its sector picks (0: this row, 45 / 135: the row below or above; 90: none):
+            // one load, by the lanes whose edge pixel can be foreground and is not 90 --
+            // instead of three edge loads per side up front (Mu / Mc / Md[0] and [5] hold 0)
+            const bool s0 = uu > 0.f, s90 = !s0 && vv > 0.f, same = (gx > 0.f) == (gy > 0.f);
+            const int up = k == 0 ? (same ? V2_CS : -V2_CS) : (same ? -V2_CS : V2_CS);
+            const bool need = (k == 0 ? left : right) && !s90;
+            const float e = need ? mc[cc0 + (k == 0 ? -1 : 4) + (s0 ? 0 : up)] : 0.f;
+            nmax = fmaxf(nmax, e);
+        }
+#endif
         const float nv = sqrt_apx(nmax);
         const float d = c - nv;
         const float e_nms = fmaf(P.e_nms_rel, c + nv, P.e_nms0);  // magnitude-relative certification band
