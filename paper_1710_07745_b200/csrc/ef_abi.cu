@@ -688,9 +688,16 @@ void fan_out_unpack(PackSlot* s);
 // among 24 ms ones, always ~56 ms late.)
 cudaError_t wait_event(cudaEvent_t ev) {
 #if EF_HOST_POLL
+    bool polled = false;
     for (;;) {
         const cudaError_t q = cudaEventQuery(ev);
-        if (q != cudaErrorNotReady) return q;
+        if (q != cudaErrorNotReady) {
+            // cudaErrorNotReady is left behind as the thread's "last error": a later
+            // cudaGetLastError() after a kernel launch (launch_pack) would report it
+            if (polled) cudaGetLastError();
+            return q;
+        }
+        polled = true;
         std::this_thread::sleep_for(std::chrono::microseconds(EF_HOST_POLL_US));
     }
 #else

@@ -508,6 +508,23 @@ def test_host_entry_edges_only(canny, shape):
         assert (big[:phase] == 7).all() and (big[phase + frames.size:] == 7).all()
 
 
+def test_host_entry_many_chunks_pageable_input(canny):
+    """A pageable input of many chunks: every chunk is staged through a pinned buffer
+    that an earlier chunk's copy may still be reading, so the call waits on copy events
+    (polling) between its kernel launches.  Results equal the device-resident call."""
+    frames = np.tile(synth.config3(4, 512), (24, 1, 1))  # 96 frames x 512^2 = 25 MB: 8 MB chunks with ramps
+    frames[::7] = frames[::7][:, ::-1].copy()
+    w = O.gaussian_weights(1.4, radius=2)
+    lab, fin = canny.canny_u8(_dev(frames), w, 20.0, 50.0)
+    for _ in range(3):  # the waits depend on timing: a few calls
+        hl, hf = canny.canny_u8_host(frames, w, 20.0, 50.0)
+        assert np.array_equal(hl, _np(lab)) and np.array_equal(hf, _np(fin))
+        _, of = canny.canny_u8_host(frames, w, 20.0, 50.0, edges_only=True)
+        assert np.array_equal(of, _np(fin))
+    el, ef_ = O.canny(frames[:4], w, 20.0, 50.0)
+    assert np.array_equal(hl[:4], el) and np.array_equal(hf[:4].astype(bool), ef_)
+
+
 def test_invalid_arguments_raise_valueerror(canny):
     w = O.gaussian_weights(1.4)
     img = _dev(np.zeros((8, 8), np.uint8))
